@@ -1,0 +1,172 @@
+/*
+ * fcwave-b200 — C ABI of the B200-native symbol-synchronized FC-F-OFDM
+ * TX synthesis / RX analysis hot path (arXiv 2008.00672).
+ *
+ * This is the drop-in boundary for the reference's operator API
+ * (/root/reference/proj/include/fcwave/fc_sync.hpp).  Every entry point names
+ * the reference interface it replaces.  Plain C types only: complex samples are
+ * interleaved float32 pairs (re, im) ("complex64"), streams are cudaStream_t
+ * passed as void*, device and host buffers are plain pointers owned by the
+ * caller.
+ *
+ * Errors: every function returns FCW_OK (0) or a status code; the message is
+ * available from fcw_last_error() (thread-local).  The codes mirror the
+ * reference's exception classes: FCW_EINVAL <-> std::invalid_argument,
+ * FCW_ERANGE <-> std::out_of_range (proj/src/fc_sync.cpp:35-38,62-63,117-125,
+ * 137-138,146-151,198-201; proj/src/numerology.cpp:45-54).
+ *
+ * Threading: a plan is immutable after creation and may be used concurrently
+ * from several host threads / CUDA streams with the device entry points
+ * (fcw_tx, fcw_rx).  The host-buffer entry points (fcw_tx_host, fcw_rx_host)
+ * serialize per plan (they own staging buffers).
+ */
+#ifndef FCWAVE_B200_H
+#define FCWAVE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FCW_OK 0
+#define FCW_EINVAL 1  /* std::invalid_argument in the reference */
+#define FCW_ERANGE 2  /* std::out_of_range in the reference */
+#define FCW_ECUDA 3   /* CUDA runtime failure (no device, launch error, ...) */
+#define FCW_ENOMEM 4  /* device / pinned host allocation failed */
+#define FCW_ENOTSUP 5 /* valid for the reference but outside this build's envelope */
+
+/* fcw_tx / fcw_rx flags */
+#define FCW_GRID_FULL 1u /* grid rows hold all L_m DFT bins per subband (QamGrid::symbols,
+                            ofdm.hpp:27-33) instead of the packed active bins */
+#define FCW_RX_FUSED 2u  /* RX by transform decomposition (rx_symbol_simplified,
+                            fc_sync.cpp:195-243); default is the direct path
+                            (rx_symbol_direct, fc_sync.cpp:158-176) */
+
+/* Geometry of one FC bank (FcParams, numerology.hpp:34-41). */
+typedef struct fcw_fc_params {
+    int L, N;
+    double overlap;
+    int L_O, L_S, L_L, L_T;
+    int N_O, N_S, N_L, N_T;
+    int I;
+} fcw_fc_params;
+
+/* One subband (SubbandConfig, fc_core.hpp:20-27, plus QamGrid::active_map,
+ * ofdm.hpp:27-33).  Copied at plan creation; the caller keeps ownership. */
+typedef struct fcw_subband {
+    int L;                  /* short transform size L_m (power of two, 4..1024, L | N) */
+    int l_ofdm;             /* OFDM transform size; must equal L (fc_sync.cpp:62-63); 0 = L */
+    int c;                  /* centre bin on the N-bin grid */
+    int n_active;           /* number of active (QAM-bearing) bins */
+    int n_tb;               /* transition bins per edge (informational) */
+    const int* active_bins; /* n_active DFT-bin indices in [0, L): packed grid order */
+    const double* window;   /* L shifted-domain weights (design_window, fc_core.cpp:25-39) */
+} fcw_subband;
+
+typedef struct fcw_plan fcw_plan;
+
+typedef struct fcw_plan_info {
+    int N, B, M;
+    double overlap;
+    int64_t Q;             /* combined_length(B) (fc_sync.cpp:90-94): waveform samples per unit */
+    int64_t useful0;       /* Waveform::useful0 of the TX output = N_L (fc_sync.cpp:102) */
+    int64_t frame_samples; /* sum_n (N + N_CP,n): air-interface samples per unit */
+    int row_active;        /* packed grid row length: sum_m n_active */
+    int row_full;          /* full grid row length: sum_m L_m */
+    int N_L, N_T;
+    int chunk;             /* symbols per CTA (launch geometry, informational) */
+} fcw_plan_info;
+
+/* ----------------------------------------------------------------- plan */
+
+/* Replaces the per-call geometry of tx_discontinuous / rx_discontinuous
+ * (fc_sync.hpp:52-54, 78-80): N, overlap, the explicit CpSchedule
+ * (numerology.hpp:23-31) and the subband configs.  Validates exactly the
+ * reference preconditions (derive_fc_params numerology.cpp:44-54,
+ * zero_pad_symbol fc_sync.cpp:35-38, tx_symbol :62-63, cp_insert ofdm.cpp:109,
+ * equal Q/useful0 across subbands fc_sync.cpp:137-138).  Allocates the
+ * device-resident tables on the current CUDA device.  flags: reserved, 0. */
+int fcw_plan_create(fcw_plan** plan, int N, double overlap, const int* cp_high, int B,
+                    const fcw_subband* subbands, int M, unsigned flags);
+void fcw_plan_destroy(fcw_plan* plan);
+int fcw_plan_get_info(const fcw_plan* plan, fcw_plan_info* info);
+/* sigma_n = n N + sum_{q=1..n} N_CP,q (symbol_sigma, fc_sync.cpp:86-88), B entries */
+int fcw_plan_sigma(const fcw_plan* plan, int64_t* sigma);
+/* per-symbol (l_cp, extrap) of subband m (cp_truncate, fc_sync.cpp:26-32), B entries each */
+int fcw_plan_cp_split(const fcw_plan* plan, int m, int* l_cp, int* extrap);
+/* subband m bin map: for shifted index p0 in [0, L): q[p0] = (c - ceil(L/2) + p0) mod N
+ * and b[p0] = (p0 + L/2) mod L (fc_core.cpp:81-84) */
+int fcw_plan_bin_map(const fcw_plan* plan, int m, int* q, int* b);
+/* rx block starts: useful0 - N_L + sigma_n (rx_segment, fc_sync.cpp:148), B entries */
+int fcw_plan_rx_starts(const fcw_plan* plan, int64_t useful0, int64_t* starts);
+int fcw_plan_fc_params(const fcw_plan* plan, int m, fcw_fc_params* out);
+
+/* ------------------------------------------------------ device entry points */
+
+/* TX synthesis of S independent units (antenna stream x frame) — replaces
+ * tx_discontinuous (fc_sync.hpp:52-54, fc_sync.cpp:114-143).
+ *   grid: device complex64 [S][B][row] with row = row_active (packed, default)
+ *         or row_full (FCW_GRID_FULL); grid_unit_stride in complex elements
+ *         (0 = B*row).
+ *   wave: device complex64 [S][wave_unit_stride] (0 = Q); samples [0, Q) of
+ *         each unit are written, useful0 = N_L.
+ * Asynchronous on `stream` (cudaStream_t; NULL = legacy default stream). */
+int fcw_tx(const fcw_plan* plan, const void* grid, int64_t grid_unit_stride, void* wave,
+           int64_t wave_unit_stride, int S, unsigned flags, void* stream);
+
+/* RX analysis of S units — replaces rx_discontinuous (fc_sync.hpp:78-80,
+ * fc_sync.cpp:245-264) for ALL subbands of the plan in one pass (one shared
+ * N-point transform per block instead of one per subband).
+ *   wave: device complex64 [S][wave_unit_stride] (0 = wave_len), wave_len
+ *         samples per unit, first useful sample of symbol 0 at useful0.
+ *   grid: device complex64 [S][B][row] (packed active bins, or all L_m bins
+ *         with FCW_GRID_FULL = the reference's return layout).
+ * flags: FCW_RX_FUSED selects the transform-decomposition path. */
+int fcw_rx(const fcw_plan* plan, const void* wave, int64_t wave_unit_stride, int64_t wave_len,
+           int64_t useful0, void* grid, int64_t grid_unit_stride, int S, unsigned flags, void* stream);
+
+/* Seeded synthetic QAM grid on the device, bit-identical to the host oracle:
+ * per unit u a splitmix64 stream seeded derive_seed(seed, unit0 + u)
+ * (channel.cpp:19-48), one draw per bit LSB-first (scenario.cpp:110-128),
+ * Gray square QAM of bits_per_symbol in {2,4,6,8} at unit power (ofdm.cpp:55-65,
+ * extended to 256-QAM).  Output: packed grid [S][B][row_active]. */
+int fcw_gen_qam(const fcw_plan* plan, uint64_t seed, int64_t unit0, int S, int bits_per_symbol,
+                void* grid, void* stream);
+
+/* -------------------------------------------------- host-buffer entry points */
+
+/* Same as fcw_tx / fcw_rx with HOST buffers (pinned via fcw_host_alloc for
+ * full PCIe overlap; pageable works but is slower).  Units are streamed in
+ * chunks through device staging buffers on two CUDA streams so H2D, kernels
+ * and D2H overlap.  Blocking. */
+int fcw_tx_host(fcw_plan* plan, const void* grid_host, void* wave_host, int S, unsigned flags);
+int fcw_rx_host(fcw_plan* plan, const void* wave_host, int64_t wave_len, int64_t useful0,
+                void* grid_host, int S, unsigned flags);
+void* fcw_host_alloc(size_t bytes);
+void fcw_host_free(void* p);
+
+/* -------------------------------------------- geometry (host, integer-exact) */
+
+int fcw_derive_fc_params(int N, int L, double overlap, fcw_fc_params* out);  /* numerology.cpp:44-70 */
+int fcw_cp_schedule(int scs_khz, int n_fft, int n_symbols, int* out);        /* numerology.cpp:29-42 */
+/* 5G-NR normal-CP pattern for scs = 15*2^mu kHz: short = 144 N/2048, long =
+ * short + 16*2^mu N/2048 on symbols n mod (7*2^mu) == 0 (0.5 ms boundaries).
+ * Equals fcw_cp_schedule at 15 kHz; gives 288/352 at 30 kHz, N=4096. */
+int fcw_nr_cp_schedule(int scs_khz, int n_fft, int n_symbols, int* out);
+int fcw_cp_truncate(int n_cp_high, int I, int* l_cp, int* extrap);           /* fc_sync.cpp:26-32 */
+int fcw_first_block_overlap(const fcw_fc_params* p, int l_cp, double* out);  /* numerology.cpp:72-76 */
+int fcw_design_window(int L, int n_pass, int n_tb, double* w);              /* fc_core.cpp:25-39 */
+int fcw_centered_active_map(int l_ofdm, int n_active, int skip_dc, int* bins); /* ofdm.cpp:80-95 */
+int64_t fcw_symbol_sigma(int n, const int* cp_high, int N);                 /* fc_sync.cpp:86-88 */
+int64_t fcw_combined_length(int B, const int* cp_high, const fcw_fc_params* p); /* fc_sync.cpp:90-94 */
+
+const char* fcw_last_error(void);
+const char* fcw_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FCWAVE_B200_H */

@@ -1,0 +1,371 @@
+"""TEST INFRASTRUCTURE ONLY — the CPU oracle for the FC-F-OFDM hot path.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and bench.py's ``cpu_baseline`` /
+``--impl reference`` legs may import this package, and only as the checker.
+The product package ``paper_2008_00672_b200`` never imports it.
+
+Two back-ends, both built by ``make -C oracle`` (see oracle/Makefile):
+
+* ``C``  — ``oracle/liboracle.so``: a plain-C double-precision restatement of
+  the reference algorithm (oracle/fcw_oracle.c; each function cites the
+  reference file:line it follows).
+* ``Ref`` — ``oracle/_ref/libfcwave_ref.so``: the UNMODIFIED reference
+  (/root/reference/proj/src/{numerology,ofdm,fc_core,fc_sync,fft}.cpp) compiled
+  against the builder-written FFTW-API shim.  Built only where /root/reference
+  exists; the .so then travels to the GPU box with the repo snapshot.
+
+Complex arrays cross the boundary as numpy complex128.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_ORACLE_SO = os.path.join(_HERE, "liboracle.so")
+_REF_SO = os.path.join(_HERE, "_ref", "libfcwave_ref.so")
+
+_i32p = np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")
+_f64p = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+_f32p = np.ctypeslib.ndpointer(dtype=np.float32, flags="C_CONTIGUOUS")
+
+
+class OracleError(RuntimeError):
+    pass
+
+
+class FcoParams(C.Structure):
+    _fields_ = [(n, C.c_int) for n in ("L", "N")] + [("overlap", C.c_double)] + [
+        (n, C.c_int) for n in ("L_O", "L_S", "L_L", "L_T", "N_O", "N_S", "N_L", "N_T", "I")
+    ]
+
+
+def build(quiet: bool = True) -> None:
+    import subprocess
+
+    subprocess.run(["make", "-C", _HERE, "-s" if quiet else "-w"], check=True)
+
+
+def _load(path):
+    if not os.path.exists(path):
+        return None
+    return C.CDLL(path)
+
+
+_lib = None
+_ref = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_ORACLE_SO):
+            build()
+        _lib = C.CDLL(_ORACLE_SO)
+        L = _lib
+        L.fco_derive_params.argtypes = [C.c_int, C.c_int, C.c_double, C.POINTER(FcoParams)]
+        L.fco_cp_schedule.argtypes = [C.c_int, C.c_int, C.c_int, _i32p]
+        L.fco_cp_truncate.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        L.fco_cp_truncate.restype = None
+        L.fco_symbol_sigma.argtypes = [C.c_int, _i32p, C.c_int]
+        L.fco_symbol_sigma.restype = C.c_int64
+        L.fco_combined_length.argtypes = [C.c_int, _i32p, C.POINTER(FcoParams)]
+        L.fco_combined_length.restype = C.c_int64
+        L.fco_design_window.argtypes = [C.c_int, C.c_int, C.c_int, _f64p]
+        L.fco_centered_active_map.argtypes = [C.c_int, C.c_int, C.c_int, _i32p]
+        for f in (L.fco_block_phase,):
+            f.argtypes = [C.c_int64, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+            f.restype = None
+        L.fco_symbol_phase.argtypes = [C.c_int, C.c_int, _i32p, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        L.fco_symbol_phase.restype = None
+        L.fco_fft.argtypes = [_f64p, C.c_int, C.c_int]
+        L.fco_fft.restype = None
+        L.fco_tx_symbol.argtypes = [_f64p, C.c_int, C.c_int, C.c_int, _f64p, C.POINTER(FcoParams), _i32p, C.c_int, _f64p]
+        L.fco_tx_discontinuous.argtypes = [
+            C.c_int, C.c_double, _i32p, C.c_int, C.c_int, _i32p, _i32p, _f64p, _f64p, _f64p,
+            C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+        L.fco_rx_block_freq.argtypes = [_f64p, C.c_int, C.c_int, _f64p, C.POINTER(FcoParams), C.c_double, C.c_double, _f64p]
+        L.fco_rx_symbol_direct.argtypes = [_f64p, _f64p, C.c_int, C.c_int, _f64p, C.POINTER(FcoParams), _i32p, C.c_int, _f64p]
+        L.fco_rx_symbol_simplified.argtypes = [_f64p, _f64p, C.POINTER(FcoParams), _f64p]
+        L.fco_rx_discontinuous.argtypes = [
+            _f64p, C.c_int64, C.c_int64, C.c_int, C.c_double, _i32p, C.c_int, C.c_int, C.c_int,
+            _f64p, C.c_int, _f64p]
+        L.fco_splitmix64.argtypes = [C.POINTER(C.c_uint64)]
+        L.fco_splitmix64.restype = C.c_uint64
+        L.fco_derive_seed.argtypes = [C.c_uint64, C.c_uint64]
+        L.fco_derive_seed.restype = C.c_uint64
+        L.fco_qam_map.argtypes = [C.c_int, C.c_uint, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        L.fco_qam_map.restype = None
+        L.fco_gen_grid.argtypes = [C.c_uint64, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int, _f64p]
+        L.fco_gen_grid.restype = None
+    return _lib
+
+
+def ref_available() -> bool:
+    return os.path.exists(_REF_SO)
+
+
+def ref():
+    global _ref
+    if _ref is None:
+        if not os.path.exists(_REF_SO):
+            raise OracleError("oracle/_ref not built (needs /root/reference at build time)")
+        _ref = C.CDLL(_REF_SO)
+        R = _ref
+        R.fcwref_last_error.restype = C.c_char_p
+        R.fcwref_tx.argtypes = [C.c_int, C.c_double, _i32p, C.c_int, C.c_int, _i32p, _i32p, _f64p, _f64p,
+                                _f64p, C.c_longlong, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong)]
+        R.fcwref_rx.argtypes = [C.c_int, C.c_double, _i32p, C.c_int, C.c_int, C.c_int, _f64p, _f64p,
+                                C.c_longlong, C.c_longlong, C.c_int, _f64p]
+        R.fcwref_tx_symbol.argtypes = [_f64p, C.c_int, C.c_int, C.c_int, _f64p, C.c_int, C.c_double, _i32p,
+                                       C.c_int, C.c_int, _f64p]
+        R.fcwref_rx_symbol_direct.argtypes = [_f64p, _f64p, C.c_int, C.c_int, _f64p, C.c_int, C.c_double,
+                                              _i32p, C.c_int, C.c_int, _f64p]
+        R.fcwref_rx_block_freq.argtypes = [_f64p, C.c_int, C.c_int, _f64p, C.c_int, C.c_double, C.c_double,
+                                           C.c_double, _f64p]
+        R.fcwref_rx_symbol_simplified.argtypes = [_f64p, _f64p, C.c_int, C.c_int, _f64p, C.c_int, C.c_double, _f64p]
+        R.fcwref_bench_txrx.argtypes = [C.c_int, C.c_double, _i32p, C.c_int, C.c_int, _i32p, _i32p, _f64p,
+                                        _i32p, _i32p, _f32p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]
+        R.fcwref_bench_txrx.restype = C.c_double
+    return _ref
+
+
+def _c128(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.complex128))
+
+
+def _as_f64(a: np.ndarray) -> np.ndarray:
+    return _c128(a).view(np.float64)
+
+
+def _i32(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.int32))
+
+
+def _check(rc: int, what: str, ref_lib=None):
+    if rc == 0:
+        return
+    msg = ""
+    if ref_lib is not None:
+        msg = ref_lib.fcwref_last_error().decode()
+    if rc == 2:
+        raise IndexError(f"{what}: out of range {msg}")
+    raise ValueError(f"{what}: invalid argument {msg}")
+
+
+# ---------------------------------------------------------------- C oracle
+@dataclass
+class Params:
+    L: int
+    N: int
+    overlap: float
+    L_O: int
+    L_S: int
+    L_L: int
+    L_T: int
+    N_O: int
+    N_S: int
+    N_L: int
+    N_T: int
+    I: int
+
+    def c(self) -> FcoParams:
+        p = FcoParams()
+        for k, v in self.__dict__.items():
+            setattr(p, k, v)
+        return p
+
+
+def derive_params(N: int, L: int, overlap: float = 0.5) -> Params:
+    p = FcoParams()
+    _check(lib().fco_derive_params(N, L, overlap, C.byref(p)), "derive_params")
+    return Params(**{k: getattr(p, k) for k, _ in FcoParams._fields_})
+
+
+def cp_schedule(scs_khz: int, n_fft: int, n_symbols: int) -> list[int]:
+    out = np.zeros(max(n_symbols, 1), np.int32)
+    _check(lib().fco_cp_schedule(scs_khz, n_fft, n_symbols, out), "cp_schedule")
+    return out.tolist()
+
+
+def cp_truncate(n_cp: int, I: int) -> tuple[int, int]:
+    a, b = C.c_int(), C.c_int()
+    lib().fco_cp_truncate(n_cp, I, C.byref(a), C.byref(b))
+    return a.value, b.value
+
+
+def symbol_sigma(n: int, cp, N: int) -> int:
+    return int(lib().fco_symbol_sigma(n, _i32(cp), N))
+
+
+def combined_length(B: int, cp, p: Params) -> int:
+    pc = p.c()
+    return int(lib().fco_combined_length(B, _i32(cp), C.byref(pc)))
+
+
+def design_window(L: int, n_pass: int, n_tb: int) -> np.ndarray:
+    w = np.zeros(L, np.float64)
+    _check(lib().fco_design_window(L, n_pass, n_tb, w), "design_window")
+    return w
+
+
+def centered_active_map(l_ofdm: int, n_active: int, skip_dc: bool = True) -> list[int]:
+    out = np.zeros(max(n_active, 1), np.int32)
+    _check(lib().fco_centered_active_map(l_ofdm, n_active, int(skip_dc), out), "centered_active_map")
+    return out[:n_active].tolist()
+
+
+def block_phase(r: int, c: int, L_S: int, L: int) -> complex:
+    a, b = C.c_double(), C.c_double()
+    lib().fco_block_phase(r, c, L_S, L, C.byref(a), C.byref(b))
+    return complex(a.value, b.value)
+
+
+def symbol_phase(n: int, c: int, cp, N: int) -> complex:
+    a, b = C.c_double(), C.c_double()
+    lib().fco_symbol_phase(n, c, _i32(cp), N, C.byref(a), C.byref(b))
+    return complex(a.value, b.value)
+
+
+def fft(x, inverse: bool = False) -> np.ndarray:
+    d = _as_f64(x).copy()
+    lib().fco_fft(d, len(d) // 2, int(inverse))
+    return d.view(np.complex128)
+
+
+def tx_symbol(sym, L: int, c: int, window, p: Params, cp, n: int) -> np.ndarray:
+    s = _as_f64(sym)
+    out = np.zeros(2 * (3 * p.N // 2), np.float64)
+    pc = p.c()
+    _check(lib().fco_tx_symbol(s, len(s) // 2, L, c, np.asarray(window, np.float64), C.byref(pc), _i32(cp), n, out),
+           "tx_symbol")
+    return out.view(np.complex128)
+
+
+def tx_discontinuous(grids, Ls, cs, windows, cp, N: int, overlap: float = 0.5):
+    """grids: list over subbands of (B, L_m) complex arrays (full columns)."""
+    B = len(cp)
+    flat = np.concatenate([_c128(g).reshape(-1) for g in grids])
+    wins = np.concatenate([np.asarray(w, np.float64) for w in windows])
+    cap = 4 * N + B * (N + max(cp) + 1) + 16
+    out = np.zeros(2 * cap, np.float64)
+    Q, u0 = C.c_int64(), C.c_int64()
+    _check(lib().fco_tx_discontinuous(N, overlap, _i32(cp), B, len(Ls), _i32(Ls), _i32(cs), wins,
+                                      flat.view(np.float64), out, cap, C.byref(Q), C.byref(u0)), "tx_discontinuous")
+    return out.view(np.complex128)[: Q.value].copy(), u0.value
+
+
+def rx_block_freq(y, L: int, c: int, window, p: Params, phase: complex) -> np.ndarray:
+    g = np.zeros(2 * L, np.float64)
+    pc = p.c()
+    lib().fco_rx_block_freq(_as_f64(y), L, c, np.asarray(window, np.float64), C.byref(pc), phase.real, phase.imag, g)
+    return g.view(np.complex128)
+
+
+def rx_symbol_direct(y0, y1, L: int, c: int, window, p: Params, cp, n: int) -> np.ndarray:
+    out = np.zeros(2 * L, np.float64)
+    pc = p.c()
+    _check(lib().fco_rx_symbol_direct(_as_f64(y0), _as_f64(y1), L, c, np.asarray(window, np.float64), C.byref(pc),
+                                      _i32(cp), n, out), "rx_symbol_direct")
+    return out.view(np.complex128)
+
+
+def rx_symbol_simplified(g0, g1, p: Params) -> np.ndarray:
+    out = np.zeros(2 * p.L, np.float64)
+    pc = p.c()
+    _check(lib().fco_rx_symbol_simplified(_as_f64(g0), _as_f64(g1), C.byref(pc), out), "rx_symbol_simplified")
+    return out.view(np.complex128)
+
+
+def rx_discontinuous(wave, useful0: int, cp, N: int, L: int, c: int, window, simplified: bool = False,
+                     overlap: float = 0.5) -> np.ndarray:
+    B = len(cp)
+    w = _as_f64(wave)
+    out = np.zeros(2 * B * L, np.float64)
+    _check(lib().fco_rx_discontinuous(w, len(w) // 2, useful0, N, overlap, _i32(cp), B, L, c,
+                                      np.asarray(window, np.float64), int(simplified), out), "rx_discontinuous")
+    return out.view(np.complex128).reshape(B, L)
+
+
+def splitmix64_stream(seed: int, n: int) -> list[int]:
+    st = C.c_uint64(seed)
+    return [int(lib().fco_splitmix64(C.byref(st))) for _ in range(n)]
+
+
+def derive_seed(seed: int, index: int) -> int:
+    return int(lib().fco_derive_seed(seed, index))
+
+
+def qam_map(bits_per_symbol: int, sym: int) -> complex:
+    a, b = C.c_double(), C.c_double()
+    lib().fco_qam_map(bits_per_symbol, sym, C.byref(a), C.byref(b))
+    return complex(a.value, b.value)
+
+
+def gen_grid(seed: int, unit0: int, units: int, B: int, A: int, bits_per_symbol: int) -> np.ndarray:
+    out = np.zeros(2 * units * B * A, np.float64)
+    lib().fco_gen_grid(seed, unit0, units, B, A, bits_per_symbol, out)
+    return out.view(np.complex128).reshape(units, B, A)
+
+
+# ------------------------------------------------------- compiled reference
+class Ref:
+    """Thin wrappers over oracle/_ref/libfcwave_ref.so (the real reference)."""
+
+    @staticmethod
+    def tx_discontinuous(grids, Ls, cs, windows, cp, N: int, overlap: float = 0.5):
+        R = ref()
+        B = len(cp)
+        flat = np.concatenate([_c128(g).reshape(-1) for g in grids])
+        wins = np.concatenate([np.asarray(w, np.float64) for w in windows])
+        cap = 4 * N + B * (N + max(cp) + 1) + 16
+        out = np.zeros(2 * cap, np.float64)
+        Q, u0 = C.c_longlong(), C.c_longlong()
+        _check(R.fcwref_tx(N, overlap, _i32(cp), B, len(Ls), _i32(Ls), _i32(cs), wins, flat.view(np.float64), out,
+                           cap, C.byref(Q), C.byref(u0)), "ref tx_discontinuous", R)
+        return out.view(np.complex128)[: Q.value].copy(), u0.value
+
+    @staticmethod
+    def rx_discontinuous(wave, useful0: int, cp, N: int, L: int, c: int, window, simplified: bool = False,
+                         overlap: float = 0.5):
+        R = ref()
+        B = len(cp)
+        w = _as_f64(wave)
+        out = np.zeros(2 * B * L, np.float64)
+        _check(R.fcwref_rx(N, overlap, _i32(cp), B, L, c, np.asarray(window, np.float64), w, len(w) // 2, useful0,
+                           int(simplified), out), "ref rx_discontinuous", R)
+        return out.view(np.complex128).reshape(B, L)
+
+    @staticmethod
+    def tx_symbol(sym, L, c, window, N, cp, n, overlap=0.5):
+        R = ref()
+        s = _as_f64(sym)
+        out = np.zeros(2 * (3 * N // 2), np.float64)
+        _check(R.fcwref_tx_symbol(s, len(s) // 2, L, c, np.asarray(window, np.float64), N, overlap, _i32(cp),
+                                  len(cp), n, out), "ref tx_symbol", R)
+        return out.view(np.complex128)
+
+    @staticmethod
+    def rx_symbol_direct(y0, y1, L, c, window, N, cp, n, overlap=0.5):
+        R = ref()
+        out = np.zeros(2 * L, np.float64)
+        _check(R.fcwref_rx_symbol_direct(_as_f64(y0), _as_f64(y1), L, c, np.asarray(window, np.float64), N,
+                                         overlap, _i32(cp), len(cp), n, out), "ref rx_symbol_direct", R)
+        return out.view(np.complex128)
+
+    @staticmethod
+    def bench_txrx(N, cp, Ls, cs, windows, n_active, active_bins, grids_packed_c64, units, threads,
+                   simplified=True, overlap=0.5):
+        R = ref()
+        g = np.ascontiguousarray(grids_packed_c64, dtype=np.complex64).view(np.float32).reshape(-1)
+        chk = C.c_double()
+        t = R.fcwref_bench_txrx(N, overlap, _i32(cp), len(cp), len(Ls), _i32(Ls), _i32(cs),
+                                np.concatenate([np.asarray(w, np.float64) for w in windows]), _i32(n_active),
+                                _i32(np.concatenate([np.asarray(b) for b in active_bins])), g, units, threads,
+                                int(simplified), C.byref(chk))
+        if t < 0:
+            raise OracleError(R.fcwref_last_error().decode())
+        return t, chk.value

@@ -1,0 +1,378 @@
+"""Python host API of fcwave-b200, mirroring the reference's operator API.
+
+Reference-shaped entry points (proj/include/fcwave/fc_sync.hpp,
+numerology.hpp, fc_core.hpp, ofdm.hpp) take and return numpy complex128 like
+the reference's std::complex<double> vectors; the work runs on the GPU through
+the C ABI.  ``Plan`` is the batched, device-resident engine that bench.py and
+production callers use: torch CUDA tensors (or raw device pointers) in and out,
+S independent (antenna stream x frame) units per call.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import FCW_GRID_FULL, FCW_RX_FUSED, check, lib
+
+
+# ------------------------------------------------------------------ geometry
+@dataclass
+class Numerology:  # numerology.hpp:14-20
+    scs_khz: int = 15
+    n_fft: int = 1024
+    symbols_per_half_subframe: int = 7
+
+    def fs_hz(self) -> float:
+        return float(self.scs_khz) * 1000.0 * self.n_fft
+
+
+@dataclass
+class CpSchedule:  # numerology.hpp:23-31
+    per_symbol_high_rate: list[int]
+
+    def total(self) -> int:
+        return int(sum(self.per_symbol_high_rate))
+
+
+@dataclass
+class FcParams:  # numerology.hpp:34-41
+    L: int
+    N: int
+    overlap: float
+    L_O: int
+    L_S: int
+    L_L: int
+    L_T: int
+    N_O: int
+    N_S: int
+    N_L: int
+    N_T: int
+    I: int
+
+    def _c(self) -> _lib.FcParamsC:
+        p = _lib.FcParamsC()
+        for k in self.__dataclass_fields__:
+            setattr(p, k, getattr(self, k))
+        return p
+
+
+@dataclass
+class SubbandConfig:  # fc_core.hpp:20-27
+    L: int
+    c: int
+    window: np.ndarray
+    n_active: int = 0
+    n_tb: int = 0
+    l_ofdm: int = 0
+
+    def __post_init__(self):
+        self.window = np.ascontiguousarray(np.asarray(self.window, dtype=np.float64))
+        if self.l_ofdm == 0:
+            self.l_ofdm = self.L
+
+
+@dataclass
+class QamGrid:  # ofdm.hpp:27-33
+    l_ofdm: int
+    active_map: list[int] = field(default_factory=list)
+    symbols: list = field(default_factory=list)  # B columns of l_ofdm complex
+
+    def n_symbols(self) -> int:
+        return len(self.symbols)
+
+
+@dataclass
+class Waveform:  # types.hpp:22-26
+    samples: np.ndarray
+    fs_hz: float = 0.0
+    useful0: int = 0
+
+
+def _i32(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.int32))
+
+
+def _i32p(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_int))
+
+
+def make_numerology(scs_khz: int, n_fft: int) -> Numerology:
+    """numerology.cpp:17-27 (validation via the C ABI)."""
+    tmp = np.zeros(1, np.int32)
+    if n_fft < 16 or n_fft & (n_fft - 1):
+        raise ValueError("n_fft must be a power of two >= 16")
+    if scs_khz <= 0 or scs_khz % 15 or (scs_khz // 15) & (scs_khz // 15 - 1):
+        raise ValueError("scs_khz must be 15*2^k")
+    del tmp
+    return Numerology(scs_khz, n_fft, 7)
+
+
+def cp_schedule(num: Numerology, n_symbols: int) -> CpSchedule:
+    out = np.zeros(max(n_symbols, 1), np.int32)
+    check(lib().fcw_cp_schedule(num.scs_khz, num.n_fft, n_symbols, _i32p(out)))
+    return CpSchedule(out.tolist())
+
+
+def nr_cp_schedule(num: Numerology, n_symbols: int) -> CpSchedule:
+    """5G-NR normal CP for any 15*2^mu kHz (288/352 at 30 kHz, N=4096)."""
+    out = np.zeros(max(n_symbols, 1), np.int32)
+    check(lib().fcw_nr_cp_schedule(num.scs_khz, num.n_fft, n_symbols, _i32p(out)))
+    return CpSchedule(out.tolist())
+
+
+def derive_fc_params(N: int, L: int, overlap: float = 0.5) -> FcParams:
+    p = _lib.FcParamsC()
+    check(lib().fcw_derive_fc_params(N, L, overlap, C.byref(p)))
+    return FcParams(**{k: getattr(p, k) for k, _ in _lib.FcParamsC._fields_})
+
+
+def first_block_overlap(p: FcParams, l_cp: int) -> float:
+    v = C.c_double()
+    pc = p._c()
+    check(lib().fcw_first_block_overlap(C.byref(pc), l_cp, C.byref(v)))
+    return v.value
+
+
+def cp_truncate(n_cp_high: int, I: int) -> tuple[int, int]:
+    a, b = C.c_int(), C.c_int()
+    check(lib().fcw_cp_truncate(n_cp_high, I, C.byref(a), C.byref(b)))
+    return a.value, b.value
+
+
+def design_window(L: int, n_pass: int, n_tb: int) -> np.ndarray:
+    w = np.zeros(max(L, 1), np.float64)
+    check(lib().fcw_design_window(L, n_pass, n_tb, w.ctypes.data_as(C.POINTER(C.c_double))))
+    return w[:L]
+
+
+def centered_active_map(l_ofdm: int, n_active: int, skip_dc: bool = True) -> list[int]:
+    b = np.zeros(max(n_active, 1), np.int32)
+    check(lib().fcw_centered_active_map(l_ofdm, n_active, int(skip_dc), _i32p(b)))
+    return b[:n_active].tolist()
+
+
+def symbol_sigma(n: int, cps: CpSchedule, N: int) -> int:
+    cp = _i32(cps.per_symbol_high_rate)
+    return int(lib().fcw_symbol_sigma(n, _i32p(cp), N))
+
+
+def combined_length(n_symbols: int, cps: CpSchedule, p: FcParams) -> int:
+    cp = _i32(cps.per_symbol_high_rate)
+    pc = p._c()
+    return int(lib().fcw_combined_length(n_symbols, _i32p(cp), C.byref(pc)))
+
+
+# ------------------------------------------------------------------- engine
+def _dev_ptr(x) -> int:
+    """Raw device pointer of a torch CUDA tensor (or pass an int through)."""
+    if isinstance(x, int):
+        return x
+    if hasattr(x, "data_ptr"):
+        if not x.is_cuda:
+            raise ValueError("device entry point needs a CUDA tensor")
+        if not x.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return x.data_ptr()
+    raise TypeError(f"unsupported buffer {type(x)}")
+
+
+def _stream_ptr(stream) -> int | None:
+    if stream is None:
+        try:
+            import torch
+
+            if torch.cuda.is_available():
+                return torch.cuda.current_stream().cuda_stream
+        except ImportError:
+            pass
+        return None
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+class Plan:
+    """Immutable device-resident FC-F-OFDM plan (fcw_plan_create).
+
+    subbands: SubbandConfig list; active_maps: per subband the active DFT bins
+    (packed grid order).  Defaults to the full L bins of each subband.
+    """
+
+    def __init__(self, N: int, cps: CpSchedule | Sequence[int], subbands: Sequence[SubbandConfig],
+                 active_maps: Sequence[Sequence[int]] | None = None, overlap: float = 0.5):
+        cp = cps.per_symbol_high_rate if isinstance(cps, CpSchedule) else list(cps)
+        self.cp = _i32(cp)
+        self.N, self.B, self.M = N, len(cp), len(subbands)
+        self.subbands = list(subbands)
+        if active_maps is None:
+            active_maps = [list(range(s.L)) for s in subbands]
+        if len(active_maps) != len(subbands):
+            raise ValueError("one active map per subband required")
+        self._bins = [_i32(a) for a in active_maps]
+        arr = (_lib.SubbandC * max(1, self.M))()
+        for m, s in enumerate(subbands):
+            if len(s.window) != s.L:
+                raise ValueError("window length must be L")
+            arr[m].L, arr[m].l_ofdm, arr[m].c = s.L, s.l_ofdm, s.c
+            arr[m].n_active, arr[m].n_tb = len(self._bins[m]), s.n_tb
+            arr[m].active_bins = _i32p(self._bins[m])
+            arr[m].window = s.window.ctypes.data_as(C.POINTER(C.c_double))
+        h = C.c_void_p()
+        check(lib().fcw_plan_create(C.byref(h), N, overlap, _i32p(self.cp), self.B, arr, self.M, 0))
+        self._h = h
+        info = _lib.PlanInfoC()
+        check(lib().fcw_plan_get_info(self._h, C.byref(info)))
+        self.Q = int(info.Q)
+        self.useful0 = int(info.useful0)
+        self.frame_samples = int(info.frame_samples)
+        self.row_active = int(info.row_active)
+        self.row_full = int(info.row_full)
+        self.N_L, self.N_T = int(info.N_L), int(info.N_T)
+        self.chunk = int(info.chunk)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib().fcw_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- geometry queries (bit-exact checks against the oracle)
+    def sigma(self) -> np.ndarray:
+        out = np.zeros(self.B, np.int64)
+        check(lib().fcw_plan_sigma(self._h, out.ctypes.data_as(C.POINTER(C.c_int64))))
+        return out
+
+    def cp_split(self, m: int) -> tuple[np.ndarray, np.ndarray]:
+        a, b = np.zeros(self.B, np.int32), np.zeros(self.B, np.int32)
+        check(lib().fcw_plan_cp_split(self._h, m, _i32p(a), _i32p(b)))
+        return a, b
+
+    def bin_map(self, m: int) -> tuple[np.ndarray, np.ndarray]:
+        L = self.subbands[m].L if 0 <= m < self.M else 1
+        q, b = np.zeros(L, np.int32), np.zeros(L, np.int32)
+        check(lib().fcw_plan_bin_map(self._h, m, _i32p(q), _i32p(b)))
+        return q, b
+
+    def rx_starts(self, useful0: int) -> np.ndarray:
+        out = np.zeros(self.B, np.int64)
+        check(lib().fcw_plan_rx_starts(self._h, useful0, out.ctypes.data_as(C.POINTER(C.c_int64))))
+        return out
+
+    def fc_params(self, m: int) -> FcParams:
+        p = _lib.FcParamsC()
+        check(lib().fcw_plan_fc_params(self._h, m, C.byref(p)))
+        return FcParams(**{k: getattr(p, k) for k, _ in _lib.FcParamsC._fields_})
+
+    def row(self, full: bool = False) -> int:
+        return self.row_full if full else self.row_active
+
+    # -- device entry points
+    def tx(self, grid, wave, S: int, full: bool = False, stream=None, grid_stride: int = 0,
+           wave_stride: int = 0) -> None:
+        check(lib().fcw_tx(self._h, _dev_ptr(grid), grid_stride, _dev_ptr(wave), wave_stride, S,
+                           FCW_GRID_FULL if full else 0, _stream_ptr(stream)))
+
+    def rx(self, wave, wave_len: int, useful0: int, grid, S: int, fused: bool = True, full: bool = False,
+           stream=None, wave_stride: int = 0, grid_stride: int = 0) -> None:
+        flags = (FCW_RX_FUSED if fused else 0) | (FCW_GRID_FULL if full else 0)
+        check(lib().fcw_rx(self._h, _dev_ptr(wave), wave_stride, wave_len, useful0, _dev_ptr(grid), grid_stride, S,
+                           flags, _stream_ptr(stream)))
+
+    def gen_qam(self, seed: int, unit0: int, S: int, bits_per_symbol: int, grid, stream=None) -> None:
+        check(lib().fcw_gen_qam(self._h, seed, unit0, S, bits_per_symbol, _dev_ptr(grid), _stream_ptr(stream)))
+
+    # -- host entry points (numpy complex64, C-contiguous)
+    def tx_host(self, grid: np.ndarray, S: int, full: bool = False, out: np.ndarray | None = None) -> np.ndarray:
+        g = np.ascontiguousarray(grid, dtype=np.complex64)
+        if g.size != S * self.B * self.row(full):
+            raise ValueError("grid size does not match S*B*row")
+        if out is None:
+            out = np.empty((S, self.Q), np.complex64)
+        check(lib().fcw_tx_host(self._h, g.ctypes.data, out.ctypes.data, S, FCW_GRID_FULL if full else 0))
+        return out
+
+    def rx_host(self, wave: np.ndarray, wave_len: int, useful0: int, S: int, fused: bool = True, full: bool = False,
+                out: np.ndarray | None = None) -> np.ndarray:
+        w = np.ascontiguousarray(wave, dtype=np.complex64)
+        if w.size != S * wave_len:
+            raise ValueError("waveform size does not match S*wave_len")
+        if out is None:
+            out = np.empty((S, self.B, self.row(full)), np.complex64)
+        flags = (FCW_RX_FUSED if fused else 0) | (FCW_GRID_FULL if full else 0)
+        check(lib().fcw_rx_host(self._h, w.ctypes.data, wave_len, useful0, out.ctypes.data, S, flags))
+        return out
+
+
+class PinnedBuffer:
+    """Page-locked host buffer (fcw_host_alloc) exposed as ``.array`` (numpy)."""
+
+    def __init__(self, shape, dtype=np.complex64):
+        n = int(np.prod(shape)) * np.dtype(dtype).itemsize
+        self._ptr = lib().fcw_host_alloc(max(n, 1))
+        if not self._ptr:
+            check(_lib.FCW_ENOMEM)
+        raw = np.ctypeslib.as_array(C.cast(self._ptr, C.POINTER(C.c_uint8)), shape=(max(n, 1),))
+        self.array = raw[:n].view(dtype).reshape(shape)
+
+    def __del__(self):
+        if getattr(self, "_ptr", None):
+            lib().fcw_host_free(self._ptr)
+            self._ptr = None
+
+
+# ------------------------------------------------- reference-shaped functions
+def _full_grid_rows(grids: Sequence[QamGrid], cfgs: Sequence[SubbandConfig], B: int) -> np.ndarray:
+    cols = []
+    for g, c in zip(grids, cfgs):
+        a = np.asarray(g.symbols, dtype=np.complex128).reshape(B, -1)
+        if a.shape[1] != c.L:
+            raise ValueError("grid column size mismatch")
+        cols.append(a)
+    return np.concatenate(cols, axis=1).astype(np.complex64)
+
+
+def tx_discontinuous(grids: Sequence[QamGrid], cfgs: Sequence[SubbandConfig], cps: CpSchedule, N: int,
+                     overlap: float, fs_hz: float) -> Waveform:
+    """fc_sync.hpp:52-54 — all subbands through ONE shared N-point transform per block."""
+    if len(grids) != len(cfgs) or not grids:
+        raise ValueError("one config per grid required")
+    B = len(cps.per_symbol_high_rate)
+    for g in grids:
+        if g.n_symbols() != B:
+            raise ValueError("grid symbol count must match CP schedule")
+    plan = Plan(N, cps, cfgs, overlap=overlap)
+    rows = _full_grid_rows(grids, cfgs, B)
+    w = plan.tx_host(rows.reshape(-1), 1, full=True)[0]
+    return Waveform(w.astype(np.complex128), fs_hz, plan.useful0)
+
+
+def rx_discontinuous_all(w: Waveform, cfgs: Sequence[SubbandConfig], cps: CpSchedule, N: int, overlap: float,
+                         simplified: bool = False) -> list[np.ndarray]:
+    """All subbands in one pass; returns per subband a (B, L) complex128 array."""
+    plan = Plan(N, cps, cfgs, overlap=overlap)
+    if simplified:
+        for c in cfgs:
+            if derive_fc_params(N, c.L, overlap).L_S * 2 != c.L:
+                raise ValueError("fused RX path requires 50 % overlap")
+    samples = np.asarray(w.samples)
+    out = plan.rx_host(samples.reshape(-1), len(samples), int(w.useful0), 1, fused=simplified, full=True)[0]
+    res, off = [], 0
+    for c in cfgs:
+        res.append(out[:, off:off + c.L].astype(np.complex128))
+        off += c.L
+    return res
+
+
+def rx_discontinuous(w: Waveform, cfg: SubbandConfig, cps: CpSchedule, N: int, overlap: float,
+                     simplified: bool = False) -> list[np.ndarray]:
+    """fc_sync.hpp:78-80 — returns B columns of L complex values."""
+    return list(rx_discontinuous_all(w, [cfg], cps, N, overlap, simplified)[0])

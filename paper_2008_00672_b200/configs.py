@@ -1,0 +1,107 @@
+"""The BASELINE.json workloads as plan specifications.
+
+Synthetic stand-ins: there is no dataset; every config is seeded random QAM on
+the allocation BASELINE.json describes.  Subband allocations are contiguous
+and centred on DC; each subband's active bins are ``centered_active_map(L,
+n_sc, skip_dc=False)`` around its centre bin, so subcarrier ``ls`` of subband
+m lands on grid bin ``c_m + ls`` (fc_core.cpp:81-84), and its window is
+``design_window(L, n_sc, n_tb)`` (fc_core.cpp:25-39).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+from . import api
+
+
+@dataclass
+class Workload:
+    name: str
+    N: int
+    scs_khz: int
+    cp: list[int]
+    subbands: list[api.SubbandConfig]
+    active_maps: list[list[int]]
+    bits_per_symbol: int
+    units: int  # independent (antenna stream x frame) units of the full workload
+    description: str
+
+    @property
+    def B(self) -> int:
+        return len(self.cp)
+
+    def plan(self) -> api.Plan:
+        return api.Plan(self.N, self.cp, self.subbands, self.active_maps)
+
+
+def _contiguous(N: int, n_sc: list[int], Ls: list[int], n_tb: int) -> tuple[list[api.SubbandConfig], list[list[int]]]:
+    total = sum(n_sc)
+    start = -(total // 2)
+    subs, maps = [], []
+    for n, L in zip(n_sc, Ls):
+        c = (start + n // 2) % N
+        subs.append(api.SubbandConfig(L=L, c=c, window=api.design_window(L, n, n_tb), n_active=n, n_tb=n_tb, l_ofdm=L))
+        maps.append(api.centered_active_map(L, n, False))
+        start += n
+    return subs, maps
+
+
+def _pow2_at_least(v: int) -> int:
+    p = 1
+    while p < v:
+        p *= 2
+    return p
+
+
+def config1() -> Workload:
+    """Mini-slot: 15 kHz, N=1024, 2 symbols, 1 PRB (12 sc), L=16, n_tb=2, QPSK."""
+    N = 1024
+    cp = api.cp_schedule(api.make_numerology(15, N), 2).per_symbol_high_rate  # [80, 72]
+    subs, maps = _contiguous(N, [12], [16], 2)
+    return Workload("c1_minislot_1prb_L16_N1024", N, 15, cp, subs, maps, 2, 65536,
+                    "15 kHz, N=1024, B=2, 1x(L=16, 12 active, n_tb=2), QPSK; batch of 65536 instances")
+
+
+def config2() -> Workload:
+    """20 MHz full slot: 15 kHz, N=2048, 14 symbols, 106 PRB = 24/24/24/34 PRB, L=512, n_tb=4, 16-QAM."""
+    N = 2048
+    cp = api.cp_schedule(api.make_numerology(15, N), 14).per_symbol_high_rate  # 160 at n%7==0, else 144
+    n_sc = [24 * 12, 24 * 12, 24 * 12, 34 * 12]
+    Ls = [_pow2_at_least(n + 8) for n in n_sc]
+    subs, maps = _contiguous(N, n_sc, Ls, 4)
+    return Workload("c2_20mhz_slot_4sb_L512_N2048", N, 15, cp, subs, maps, 4, 1024,
+                    "15 kHz, N=2048, B=14, 4x(L=512, 288/288/288/408 active, n_tb=4), 16-QAM")
+
+
+def config4(streams: int = 4) -> Workload:
+    """100 MHz frame: 30 kHz, N=4096, 280 symbols, 273 x 1-PRB subbands, L=16, 256-QAM, 4 streams."""
+    N = 4096
+    cp = api.nr_cp_schedule(api.make_numerology(30, N), 280).per_symbol_high_rate  # 352 every 14, else 288
+    subs, maps = _contiguous(N, [12] * 273, [16] * 273, 2)
+    return Workload("c4_100mhz_frame_273sb_L16_N4096", N, 30, cp, subs, maps, 8, streams,
+                    "30 kHz, N=4096, B=280, 273x(L=16, 12 active, n_tb=2), 256-QAM, 4 antenna streams")
+
+
+def config5(streams: int = 64, frames: int = 8) -> Workload:
+    """Multi-antenna sweep: 30 kHz, N=4096, 280 symbols, 22x12 PRB + 1x9 PRB subbands, L=256, 256-QAM."""
+    N = 4096
+    cp = api.nr_cp_schedule(api.make_numerology(30, N), 280).per_symbol_high_rate
+    subs, maps = _contiguous(N, [144] * 22 + [108], [256] * 23, 4)
+    return Workload("c5_100mhz_64ant_x8frames_23sb_L256_N4096", N, 30, cp, subs, maps, 8, streams * frames,
+                    "30 kHz, N=4096, B=280, 22x(L=256,144 active)+1x(L=256,108 active), n_tb=4, 256-QAM, "
+                    "64 antenna streams x 8 frames")
+
+
+CONFIGS = {"c1": config1, "c2": config2, "c4": config4, "c5": config5}
+
+
+def get(name: str, **kw) -> Workload:
+    return CONFIGS[name](**kw)
+
+
+def algorithmic_bytes_per_unit(w: Workload, row_active: int, Q: int) -> dict:
+    """TX reads the packed grid and writes Q samples; RX reads
+    Q samples and writes the packed grid; complex fp32 = 8 B."""
+    grid = 8 * w.B * row_active
+    wave = 8 * Q
+    return {"tx": grid + wave, "rx": grid + wave, "total": 2 * (grid + wave)}

@@ -1,0 +1,696 @@
+// Host side of the C ABI (include/fcwave_b200.h): integer-exact geometry, the
+// immutable device-resident plan, launch configuration and the pipelined
+// host-buffer entry points.  Reference anchors are cited per function.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "fcw_internal.hpp"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+    g_err = std::string(where) + ": " + cudaGetErrorString(e);
+    return e == cudaErrorMemoryAllocation ? FCW_ENOMEM : FCW_ECUDA;
+}
+
+bool is_pow2(long long v) { return v >= 1 && (v & (v - 1)) == 0; }
+int ilog2(long long v) {
+    int l = 0;
+    while ((1LL << l) < v) ++l;
+    return l;
+}
+long long mod_ll(long long a, long long m) {
+    long long r = a % m;
+    return r < 0 ? r + m : r;
+}
+
+// numerology.cpp:44-70
+int derive(int N, int L, double overlap, fcw_fc_params* p) {
+    if (L < 2 || N < L || N % L != 0) return fail(FCW_EINVAL, "L must divide N");
+    const double lo = overlap * L;
+    const int L_O = (int)std::lround(lo);
+    if (std::fabs(lo - L_O) > 1e-9 || L_O <= 0 || L_O >= L)
+        return fail(FCW_EINVAL, "overlap*L must be a positive integer < L");
+    const double no = overlap * N;
+    const int N_O = (int)std::lround(no);
+    if (std::fabs(no - N_O) > 1e-9) return fail(FCW_EINVAL, "overlap*N must be an integer");
+    p->L = L;
+    p->N = N;
+    p->overlap = overlap;
+    p->I = N / L;
+    p->L_O = L_O;
+    p->L_S = L - L_O;
+    p->L_L = (L_O + 1) / 2;
+    p->L_T = L_O / 2;
+    p->N_O = N_O;
+    p->N_S = N - N_O;
+    p->N_L = (N_O + 1) / 2;
+    p->N_T = N_O / 2;
+    return FCW_OK;
+}
+
+long long cp_partial(const std::vector<int>& cp, int n) {
+    long long s = 0;
+    for (int q = 1; q <= n; ++q) s += cp[q];
+    return s;
+}
+
+int pick_chunk(const fcw::Plan& p, int S) {
+    if (const char* e = std::getenv("FCW_CHUNK")) {
+        const int c = std::atoi(e);
+        if (c > 0) return std::min(c, p.B);
+    }
+    // enough CTAs for ~16 waves at one CTA per SM, but long enough runs to
+    // amortise the one recomputed symbol per TX chunk
+    const long long target = 16LL * 148;
+    long long per_unit = (target + S - 1) / std::max(S, 1);
+    if (per_unit < 1) per_unit = 1;
+    int chunk = (int)((p.B + per_unit - 1) / per_unit);
+    chunk = std::max(chunk, std::min(p.B, 8));
+    return std::min(chunk, p.B);
+}
+
+}  // namespace
+
+struct fcw_plan : fcw::Plan {};
+
+extern "C" {
+
+const char* fcw_last_error(void) { return g_err.c_str(); }
+const char* fcw_version(void) { return "fcwave-b200 0.1 (sm_100a)"; }
+
+int fcw_derive_fc_params(int N, int L, double overlap, fcw_fc_params* out) {
+    if (!out) return fail(FCW_EINVAL, "null output");
+    return derive(N, L, overlap, out);
+}
+
+// numerology.cpp:17-42
+int fcw_cp_schedule(int scs_khz, int n_fft, int n_symbols, int* out) {
+    if (!is_pow2(n_fft) || n_fft < 16) return fail(FCW_EINVAL, "n_fft must be a power of two >= 16");
+    if (scs_khz <= 0 || scs_khz % 15 != 0 || !is_pow2(scs_khz / 15))
+        return fail(FCW_EINVAL, "scs_khz must be 15*2^k");
+    if (n_symbols < 1) return fail(FCW_EINVAL, "n_symbols must be >= 1");
+    if ((80LL * n_fft) % 1024 != 0 || (72LL * n_fft) % 1024 != 0)
+        return fail(FCW_EINVAL, "n_fft does not scale the CP pattern to integers");
+    for (int n = 0; n < n_symbols; ++n) out[n] = (int)((n % 7 == 0 ? 80LL : 72LL) * n_fft / 1024);
+    return FCW_OK;
+}
+
+int fcw_nr_cp_schedule(int scs_khz, int n_fft, int n_symbols, int* out) {
+    if (!is_pow2(n_fft) || n_fft < 16) return fail(FCW_EINVAL, "n_fft must be a power of two >= 16");
+    if (scs_khz <= 0 || scs_khz % 15 != 0 || !is_pow2(scs_khz / 15))
+        return fail(FCW_EINVAL, "scs_khz must be 15*2^k");
+    if (n_symbols < 1) return fail(FCW_EINVAL, "n_symbols must be >= 1");
+    const long long mu2 = scs_khz / 15;  // 2^mu
+    if ((144LL * n_fft) % 2048 != 0 || (16LL * mu2 * n_fft) % 2048 != 0)
+        return fail(FCW_EINVAL, "n_fft does not scale the CP pattern to integers");
+    const int short_cp = (int)(144LL * n_fft / 2048);
+    const int long_cp = short_cp + (int)(16LL * mu2 * n_fft / 2048);
+    const long long period = 7 * mu2;
+    for (int n = 0; n < n_symbols; ++n) out[n] = (n % period == 0) ? long_cp : short_cp;
+    return FCW_OK;
+}
+
+int fcw_cp_truncate(int n_cp_high, int I, int* l_cp, int* extrap) {
+    if (I < 1) return fail(FCW_EINVAL, "interpolation factor must be >= 1");
+    *l_cp = n_cp_high / I;
+    *extrap = n_cp_high - I * *l_cp;
+    return FCW_OK;
+}
+
+int fcw_first_block_overlap(const fcw_fc_params* p, int l_cp, double* out) {
+    if (l_cp < 0 || l_cp > p->L_L) return fail(FCW_EINVAL, "CP does not fit in the leading overlap (L_CP > L_L)");
+    *out = 0.5 - (double)l_cp / p->L;
+    return FCW_OK;
+}
+
+int fcw_design_window(int L, int n_pass, int n_tb, double* w) {
+    if (n_pass <= 0 || n_tb < 0 || n_pass + 2 * n_tb > L) return fail(FCW_EINVAL, "window allocation exceeds L");
+    for (int i = 0; i < L; ++i) w[i] = 0.0;
+    const int lo = L / 2 - n_pass / 2, hi = lo + n_pass - 1;
+    for (int i = lo; i <= hi; ++i) w[i] = 1.0;
+    for (int k = 0; k < n_tb; ++k) {
+        const double v = std::cos(M_PI * (k + 1) / (2.0 * (n_tb + 1)));
+        w[lo - 1 - k] = v * v;
+        w[hi + 1 + k] = v * v;
+    }
+    return FCW_OK;
+}
+
+int fcw_centered_active_map(int l_ofdm, int n_active, int skip_dc, int* bins) {
+    if (n_active <= 0 || n_active > l_ofdm - (skip_dc ? 1 : 0))
+        return fail(FCW_EINVAL, "active subcarriers do not fit the transform");
+    int k = 0;
+    const int lo = n_active / 2;
+    if (skip_dc) {
+        for (int ls = -lo; ls <= -1; ++ls) bins[k++] = (ls + l_ofdm) % l_ofdm;
+        for (int ls = 1; ls <= n_active - lo; ++ls) bins[k++] = ls;
+    } else {
+        for (int ls = -lo; ls < n_active - lo; ++ls) bins[k++] = (ls + l_ofdm) % l_ofdm;
+    }
+    return FCW_OK;
+}
+
+int64_t fcw_symbol_sigma(int n, const int* cp, int N) {
+    int64_t s = (int64_t)n * N;
+    for (int q = 1; q <= n; ++q) s += cp[q];
+    return s;
+}
+
+int64_t fcw_combined_length(int B, const int* cp, const fcw_fc_params* p) {
+    int64_t q = (int64_t)p->N_L + p->N_T + (int64_t)B * p->N;
+    for (int i = 1; i <= B - 1; ++i) q += cp[i];
+    return q;
+}
+
+void* fcw_host_alloc(size_t bytes) {
+    void* p = nullptr;
+    const cudaError_t e = cudaMallocHost(&p, bytes);
+    if (e != cudaSuccess) {
+        cuda_fail(e, "cudaMallocHost");
+        return nullptr;
+    }
+    return p;
+}
+
+void fcw_host_free(void* p) {
+    if (p) cudaFreeHost(p);
+}
+
+// ------------------------------------------------------------------- plan
+
+int fcw_plan_create(fcw_plan** out, int N, double overlap, const int* cp_high, int B,
+                    const fcw_subband* sbs, int M, unsigned flags) {
+    (void)flags;
+    if (!out) return fail(FCW_EINVAL, "null plan pointer");
+    *out = nullptr;
+    if (M < 1 || !sbs) return fail(FCW_EINVAL, "one config per grid required");
+    if (B < 1 || !cp_high) return fail(FCW_EINVAL, "no symbols");
+    for (int n = 0; n < B; ++n)
+        if (cp_high[n] < 0) return fail(FCW_EINVAL, "negative CP length");
+    // Reference-valid geometry first (same messages as the reference) ...
+    std::vector<fcw_fc_params> ps(M);
+    for (int m = 0; m < M; ++m) {
+        const fcw_subband& s = sbs[m];
+        if (s.l_ofdm != 0 && s.l_ofdm != s.L)
+            return fail(FCW_EINVAL, "symbol-synchronized TX requires L == L_OFDM");
+        if (!s.window) return fail(FCW_EINVAL, "window length must be L");
+        if (int rc = derive(N, s.L, overlap, &ps[m])) return rc;
+        if (s.n_active < 0 || (s.n_active > 0 && !s.active_bins))
+            return fail(FCW_EINVAL, "active bins missing");
+        for (int a = 0; a < s.n_active; ++a)
+            if (s.active_bins[a] < 0 || s.active_bins[a] >= s.L)
+                return fail(FCW_EINVAL, "active bin outside [0, L)");
+        for (int n = 0; n < B; ++n) {
+            const int lcp = cp_high[n] / ps[m].I;
+            if (lcp > ps[m].L_L) return fail(FCW_EINVAL, "CP exceeds leading overlap (L_CP > L_L)");
+            if (lcp >= s.L) return fail(FCW_EINVAL, "l_cp out of range");
+        }
+        if (ps[m].N_L != ps[0].N_L || ps[m].N_T != ps[0].N_T)
+            return fail(FCW_EINVAL, "subbands must share N and the overlap factor");
+    }
+    // ... then this build's envelope.
+    if (overlap != 0.5)
+        return fail(FCW_ENOTSUP, "symbol-synchronized path is built for overlap 0.5 (the reference's only "
+                                 "consistent setting: combine_symbols writes 3N/2 per symbol)");
+    if (!is_pow2(N) || N < 16 || N > fcw::kMaxN) return fail(FCW_ENOTSUP, "N must be a power of two in [16, 4096]");
+    for (int m = 0; m < M; ++m)
+        if (!is_pow2(sbs[m].L) || sbs[m].L < 4 || sbs[m].L > fcw::kMaxL)
+            return fail(FCW_ENOTSUP, "L must be a power of two in [4, 1024]");
+
+    fcw_plan* p = new (std::nothrow) fcw_plan();
+    if (!p) return fail(FCW_ENOMEM, "host allocation failed");
+    cudaGetDevice(&p->device);
+    p->N = N;
+    p->B = B;
+    p->M = M;
+    p->overlap = overlap;
+    p->pN = ps[0];
+    p->cp.assign(cp_high, cp_high + B);
+    p->sigma.resize(B);
+    for (int n = 0; n < B; ++n) p->sigma[n] = (long long)n * N + cp_partial(p->cp, n);
+    p->Q = (long long)ps[0].N_L + ps[0].N_T + (long long)B * N + cp_partial(p->cp, B - 1);
+    p->useful0 = ps[0].N_L;
+    p->frame_samples = 0;
+    for (int n = 0; n < B; ++n) p->frame_samples += N + p->cp[n];
+
+    // subbands, tables
+    p->subs.resize(M);
+    int act_off = 0, full_off = 0;
+    std::vector<int> cnt(N, 0);
+    struct Contrib {
+        int m, p0, q, rank;
+    };
+    std::vector<Contrib> secondary;
+    p->h_inv.assign(0, 0);
+    for (int m = 0; m < M; ++m) {
+        const fcw_subband& s = sbs[m];
+        auto& S = p->subs[m];
+        S.desc = s;
+        S.bins.assign(s.active_bins, s.active_bins + s.n_active);
+        S.window.assign(s.window, s.window + s.L);
+        S.p = ps[m];
+        S.desc.active_bins = nullptr;
+        S.desc.window = nullptr;
+        fcw::SubDev d{};
+        d.L = s.L;
+        d.logL = ilog2(s.L);
+        d.c = s.c;
+        d.logI = ilog2(ps[m].I);
+        d.act_off = act_off;
+        d.n_act = s.n_active;
+        d.full_off = full_off;
+        d.cmodN = (int)mod_ll(s.c, N);
+        // block_phase(1, c, L_S, L) with L_S = L/2: exp(j*pi*(c mod 2))
+        d.bp1 = (mod_ll((long long)mod_ll(s.c, s.L) * ps[m].L_S, s.L) == 0) ? 1.0f : -1.0f;
+        d.tx_scale = (float)(std::sqrt((double)ps[m].I) / ((double)N * std::sqrt((double)s.L)));
+        d.rx_s0 = (float)(std::sqrt((double)ps[m].I) * ((double)s.L / N) / std::sqrt((double)s.L));
+        p->h_sub.push_back(d);
+        std::vector<int> inv(s.L, -1);
+        for (int a = 0; a < s.n_active; ++a) {
+            if (inv[s.active_bins[a]] >= 0) {
+                delete p;
+                return fail(FCW_EINVAL, "duplicate active bin");
+            }
+            inv[s.active_bins[a]] = a;
+        }
+        for (int b = 0; b < s.L; ++b) p->h_inv.push_back(inv[b]);
+        for (int p0 = 0; p0 < s.L; ++p0) {
+            p->h_win.push_back((float)s.window[p0]);
+            const int q = (int)mod_ll((long long)s.c - (s.L + 1) / 2 + p0, N);
+            if (s.window[p0] == 0.0) {
+                p->h_dest.push_back(-1);
+            } else if (cnt[q] == 0) {
+                p->h_dest.push_back(q);
+                cnt[q] = 1;
+            } else {
+                secondary.push_back({m, p0, q, cnt[q]});
+                cnt[q] += 1;
+                p->h_dest.push_back(-2);  // patched below
+            }
+        }
+        act_off += s.n_active;
+        full_off += s.L;
+        p->Lmax = std::max(p->Lmax, s.L);
+    }
+    p->row_active = act_off;
+    p->row_full = full_off;
+    // secondary contributions: ext slots ordered by rank (level), then by order
+    std::stable_sort(secondary.begin(), secondary.end(),
+                     [](const Contrib& a, const Contrib& b) { return a.rank < b.rank; });
+    int max_rank = secondary.empty() ? 0 : secondary.back().rank;
+    if (max_rank > fcw::kMaxLevels) {
+        delete p;
+        return fail(FCW_ENOTSUP, "more than 9 subbands share one N-grid bin");
+    }
+    p->n_ext = (int)secondary.size();
+    p->n_lvl = max_rank;
+    p->lvl_start.assign(max_rank + 1, 0);
+    for (int k = 0; k < p->n_ext; ++k) {
+        const Contrib& c = secondary[k];
+        p->h_dest[p->h_sub[c.m].full_off + c.p0] = N + k;
+        p->h_fix.push_back(c.q);
+    }
+    for (int l = 0; l <= max_rank; ++l) {
+        int k = 0;
+        while (k < p->n_ext && secondary[k].rank < l + 1) ++k;
+        p->lvl_start[l] = k;
+    }
+    for (int q = 0; q < N; ++q)
+        if (cnt[q] == 0) p->h_zero.push_back(q);
+    // L groups
+    std::map<int, std::vector<int>> groups;
+    for (int m = 0; m < M; ++m) groups[sbs[m].L].push_back(m);
+    p->n_groups = 0;
+    for (auto& kv : groups) {
+        p->grp_L[p->n_groups] = kv.first;
+        p->grp_start[p->n_groups] = (int)p->h_grp_sub.size();
+        p->grp_count[p->n_groups] = (int)kv.second.size();
+        for (int m : kv.second) p->h_grp_sub.push_back(m);
+        ++p->n_groups;
+    }
+    // symbols
+    p->h_sym.resize(B);
+    for (int n = 0; n < B; ++n) {
+        fcw::SymDev s{};
+        s.sigma = p->sigma[n];
+        s.cp = p->cp[n];
+        s.own_len = (n < B - 1) ? N + p->cp[n + 1] : 3 * N / 2;
+        s.carry_len = n > 0 ? N / 2 - p->cp[n] : 0;
+        s.smodN = (int)mod_ll(cp_partial(p->cp, n), N);
+        p->h_sym[n] = s;
+    }
+    // device tables in one blob
+    std::vector<float2> tw(N);
+    for (int k = 0; k < N; ++k) {
+        const double a = -2.0 * M_PI * (double)k / N;
+        tw[k] = make_float2((float)std::cos(a), (float)std::sin(a));
+    }
+    auto align = [](size_t v) { return (v + 255) & ~size_t(255); };
+    size_t off = 0;
+    const size_t o_sub = off;
+    off = align(off + sizeof(fcw::SubDev) * M);
+    const size_t o_sym = off;
+    off = align(off + sizeof(fcw::SymDev) * B);
+    const size_t o_win = off;
+    off = align(off + sizeof(float) * p->h_win.size());
+    const size_t o_inv = off;
+    off = align(off + sizeof(int) * p->h_inv.size());
+    const size_t o_dest = off;
+    off = align(off + sizeof(int) * p->h_dest.size());
+    const size_t o_grp = off;
+    off = align(off + sizeof(int) * p->h_grp_sub.size());
+    const size_t o_fix = off;
+    off = align(off + sizeof(int) * std::max<size_t>(1, p->h_fix.size()));
+    const size_t o_zero = off;
+    off = align(off + sizeof(int) * std::max<size_t>(1, p->h_zero.size()));
+    const size_t o_tw = off;
+    off = align(off + sizeof(float2) * N);
+    std::vector<unsigned char> host(off, 0);
+    std::memcpy(&host[o_sub], p->h_sub.data(), sizeof(fcw::SubDev) * M);
+    std::memcpy(&host[o_sym], p->h_sym.data(), sizeof(fcw::SymDev) * B);
+    std::memcpy(&host[o_win], p->h_win.data(), sizeof(float) * p->h_win.size());
+    std::memcpy(&host[o_inv], p->h_inv.data(), sizeof(int) * p->h_inv.size());
+    std::memcpy(&host[o_dest], p->h_dest.data(), sizeof(int) * p->h_dest.size());
+    std::memcpy(&host[o_grp], p->h_grp_sub.data(), sizeof(int) * p->h_grp_sub.size());
+    if (!p->h_fix.empty()) std::memcpy(&host[o_fix], p->h_fix.data(), sizeof(int) * p->h_fix.size());
+    if (!p->h_zero.empty()) std::memcpy(&host[o_zero], p->h_zero.data(), sizeof(int) * p->h_zero.size());
+    std::memcpy(&host[o_tw], tw.data(), sizeof(float2) * N);
+    cudaError_t e = cudaMalloc(&p->d_blob, off);
+    if (e != cudaSuccess) {
+        delete p;
+        return cuda_fail(e, "cudaMalloc(plan tables)");
+    }
+    e = cudaMemcpy(p->d_blob, host.data(), off, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        cudaFree(p->d_blob);
+        delete p;
+        return cuda_fail(e, "cudaMemcpy(plan tables)");
+    }
+    auto* base = static_cast<unsigned char*>(p->d_blob);
+    p->d_sub = reinterpret_cast<fcw::SubDev*>(base + o_sub);
+    p->d_sym = reinterpret_cast<fcw::SymDev*>(base + o_sym);
+    p->d_win = reinterpret_cast<float*>(base + o_win);
+    p->d_inv = reinterpret_cast<int*>(base + o_inv);
+    p->d_dest = reinterpret_cast<int*>(base + o_dest);
+    p->d_grp_sub = reinterpret_cast<int*>(base + o_grp);
+    p->d_fix = reinterpret_cast<int*>(base + o_fix);
+    p->d_zero = reinterpret_cast<int*>(base + o_zero);
+    p->d_tw = reinterpret_cast<float2*>(base + o_tw);
+    // SMEM envelope check (one CTA must fit)
+    int dev_smem = 0;
+    cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, p->device);
+    const size_t need = std::max(fcw::tx_smem_bytes(*p), fcw::rx_smem_bytes(*p));
+    if ((size_t)dev_smem < need) {
+        cudaFree(p->d_blob);
+        delete p;
+        return fail(FCW_ENOTSUP, "plan exceeds the per-CTA shared-memory envelope");
+    }
+    p->chunk = pick_chunk(*p, 1);
+    *out = p;
+    return FCW_OK;
+}
+
+void fcw_plan_destroy(fcw_plan* p) {
+    if (!p) return;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(p->device);
+    for (int i = 0; i < 2; ++i) {
+        for (int j = 0; j < 2; ++j)
+            if (p->stage[i][j]) cudaFree(p->stage[i][j]);
+        if (p->streams[i]) cudaStreamDestroy(p->streams[i]);
+    }
+    if (p->d_blob) cudaFree(p->d_blob);
+    cudaSetDevice(cur);
+    delete p;
+}
+
+int fcw_plan_get_info(const fcw_plan* p, fcw_plan_info* info) {
+    if (!p || !info) return fail(FCW_EINVAL, "null argument");
+    info->N = p->N;
+    info->B = p->B;
+    info->M = p->M;
+    info->overlap = p->overlap;
+    info->Q = p->Q;
+    info->useful0 = p->useful0;
+    info->frame_samples = p->frame_samples;
+    info->row_active = p->row_active;
+    info->row_full = p->row_full;
+    info->N_L = p->pN.N_L;
+    info->N_T = p->pN.N_T;
+    info->chunk = p->chunk;
+    return FCW_OK;
+}
+
+int fcw_plan_sigma(const fcw_plan* p, int64_t* sigma) {
+    if (!p || !sigma) return fail(FCW_EINVAL, "null argument");
+    for (int n = 0; n < p->B; ++n) sigma[n] = p->sigma[n];
+    return FCW_OK;
+}
+
+int fcw_plan_cp_split(const fcw_plan* p, int m, int* l_cp, int* extrap) {
+    if (!p || !l_cp || !extrap) return fail(FCW_EINVAL, "null argument");
+    if (m < 0 || m >= p->M) return fail(FCW_ERANGE, "subband index");
+    const int I = p->subs[m].p.I;
+    for (int n = 0; n < p->B; ++n) {
+        l_cp[n] = p->cp[n] / I;
+        extrap[n] = p->cp[n] - I * l_cp[n];
+    }
+    return FCW_OK;
+}
+
+int fcw_plan_bin_map(const fcw_plan* p, int m, int* q, int* b) {
+    if (!p) return fail(FCW_EINVAL, "null argument");
+    if (m < 0 || m >= p->M) return fail(FCW_ERANGE, "subband index");
+    const auto& s = p->subs[m];
+    const int L = s.desc.L;
+    for (int p0 = 0; p0 < L; ++p0) {
+        if (q) q[p0] = (int)mod_ll((long long)s.desc.c - (L + 1) / 2 + p0, p->N);
+        if (b) b[p0] = (p0 + L / 2) % L;
+    }
+    return FCW_OK;
+}
+
+int fcw_plan_rx_starts(const fcw_plan* p, int64_t useful0, int64_t* starts) {
+    if (!p || !starts) return fail(FCW_EINVAL, "null argument");
+    for (int n = 0; n < p->B; ++n) starts[n] = useful0 - p->pN.N_L + p->sigma[n];
+    return FCW_OK;
+}
+
+int fcw_plan_fc_params(const fcw_plan* p, int m, fcw_fc_params* out) {
+    if (!p || !out) return fail(FCW_EINVAL, "null argument");
+    if (m < 0 || m >= p->M) return fail(FCW_ERANGE, "subband index");
+    *out = p->subs[m].p;
+    return FCW_OK;
+}
+
+// --------------------------------------------------------- device entry points
+
+int fcw_tx(const fcw_plan* p, const void* grid, int64_t grid_stride, void* wave, int64_t wave_stride, int S,
+           unsigned flags, void* stream) {
+    if (!p) return fail(FCW_EINVAL, "null plan");
+    if (S < 0) return fail(FCW_EINVAL, "negative unit count");
+    if (S == 0) return FCW_OK;
+    if (!grid || !wave) return fail(FCW_EINVAL, "null buffer");
+    const int row = (flags & FCW_GRID_FULL) ? p->row_full : p->row_active;
+    if (grid_stride == 0) grid_stride = (int64_t)p->B * row;
+    if (wave_stride == 0) wave_stride = p->Q;
+    if (grid_stride < (int64_t)p->B * row) return fail(FCW_EINVAL, "grid unit stride too small");
+    if (wave_stride < p->Q) return fail(FCW_EINVAL, "waveform unit stride smaller than Q");
+    fcw::KParams kp{};
+    fcw::fill_common(*p, kp);
+    kp.chunk = pick_chunk(*p, S);
+    kp.nchunks = (p->B + kp.chunk - 1) / kp.chunk;
+    kp.row_len = row;
+    kp.grid_full = (flags & FCW_GRID_FULL) ? 1 : 0;
+    kp.in = static_cast<const float2*>(grid);
+    kp.in_stride = grid_stride;
+    kp.out = static_cast<float2*>(wave);
+    kp.out_stride = wave_stride;
+    const cudaError_t e = fcw::launch_tx(*p, kp, S, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "tx launch");
+    return FCW_OK;
+}
+
+int fcw_rx(const fcw_plan* p, const void* wave, int64_t wave_stride, int64_t wave_len, int64_t useful0,
+           void* grid, int64_t grid_stride, int S, unsigned flags, void* stream) {
+    if (!p) return fail(FCW_EINVAL, "null plan");
+    if (S < 0) return fail(FCW_EINVAL, "negative unit count");
+    if (S == 0) return FCW_OK;
+    if (!grid || !wave) return fail(FCW_EINVAL, "null buffer");
+    if (wave_stride == 0) wave_stride = wave_len;
+    if (wave_stride < wave_len) return fail(FCW_EINVAL, "waveform unit stride smaller than its length");
+    // rx_segment bounds (fc_sync.cpp:146-151), checked for every symbol
+    for (int n = 0; n < p->B; ++n) {
+        const long long start = useful0 - p->pN.N_L + p->sigma[n];
+        if (start < 0 || start + 3LL * p->N / 2 > wave_len)
+            return fail(FCW_EINVAL, "waveform too short for symbol window");
+    }
+    const int row = (flags & FCW_GRID_FULL) ? p->row_full : p->row_active;
+    if (grid_stride == 0) grid_stride = (int64_t)p->B * row;
+    if (grid_stride < (int64_t)p->B * row) return fail(FCW_EINVAL, "grid unit stride too small");
+    fcw::KParams kp{};
+    fcw::fill_common(*p, kp);
+    kp.chunk = pick_chunk(*p, S);
+    kp.nchunks = (p->B + kp.chunk - 1) / kp.chunk;
+    kp.row_len = row;
+    kp.grid_full = (flags & FCW_GRID_FULL) ? 1 : 0;
+    kp.fused = (flags & FCW_RX_FUSED) ? 1 : 0;
+    kp.rx_base = useful0 - p->pN.N_L;
+    kp.wave_len = wave_len;
+    kp.in = static_cast<const float2*>(wave);
+    kp.in_stride = wave_stride;
+    kp.out = static_cast<float2*>(grid);
+    kp.out_stride = grid_stride;
+    const cudaError_t e = fcw::launch_rx(*p, kp, S, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "rx launch");
+    return FCW_OK;
+}
+
+int fcw_gen_qam(const fcw_plan* p, uint64_t seed, int64_t unit0, int S, int bits, void* grid, void* stream) {
+    if (!p || !grid) return fail(FCW_EINVAL, "null argument");
+    if (bits != 2 && bits != 4 && bits != 6 && bits != 8) return fail(FCW_EINVAL, "bits_per_symbol must be 2,4,6,8");
+    if (S <= 0) return FCW_OK;
+    const cudaError_t e =
+        fcw::launch_gen_qam(*p, seed, unit0, S, bits, static_cast<float2*>(grid), static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "gen_qam launch");
+    return FCW_OK;
+}
+
+// ------------------------------------------------------ host-buffer pipeline
+
+namespace {
+
+int ensure_stage(fcw_plan* p, int set, int which, size_t bytes) {
+    if (p->stage_bytes[set][which] >= bytes) return FCW_OK;
+    if (p->stage[set][which]) cudaFree(p->stage[set][which]);
+    p->stage[set][which] = nullptr;
+    p->stage_bytes[set][which] = 0;
+    cudaError_t e = cudaMalloc(&p->stage[set][which], bytes);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(staging)");
+    p->stage_bytes[set][which] = bytes;
+    return FCW_OK;
+}
+
+int ensure_streams(fcw_plan* p) {
+    for (int i = 0; i < 2; ++i)
+        if (!p->streams[i]) {
+            cudaError_t e = cudaStreamCreateWithFlags(&p->streams[i], cudaStreamNonBlocking);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
+        }
+    return FCW_OK;
+}
+
+// Units per pipeline chunk: ~256 MiB of staging per direction and set.
+int units_per_chunk(size_t in_unit, size_t out_unit, int S) {
+    const size_t budget = 256u << 20;
+    size_t u = budget / std::max<size_t>(1, std::max(in_unit, out_unit));
+    if (u < 1) u = 1;
+    // at least 4 chunks when there is enough work, so copies overlap kernels
+    const size_t quarter = (S + 3) / 4;
+    if (quarter >= 1 && u > quarter) u = quarter;
+    return (int)std::min<size_t>(u, (size_t)S);
+}
+
+}  // namespace
+
+int fcw_tx_host(fcw_plan* p, const void* grid_host, void* wave_host, int S, unsigned flags) {
+    if (!p) return fail(FCW_EINVAL, "null plan");
+    if (S <= 0) return S == 0 ? FCW_OK : fail(FCW_EINVAL, "negative unit count");
+    if (!grid_host || !wave_host) return fail(FCW_EINVAL, "null buffer");
+    std::lock_guard<std::mutex> lk(p->host_mu);
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(p->device);
+    const int row = (flags & FCW_GRID_FULL) ? p->row_full : p->row_active;
+    const size_t in_unit = sizeof(float2) * (size_t)p->B * row;
+    const size_t out_unit = sizeof(float2) * (size_t)p->Q;
+    const int U = units_per_chunk(in_unit, out_unit, S);
+    int rc = ensure_streams(p);
+    for (int s = 0; rc == FCW_OK && s < 2; ++s) {
+        rc = ensure_stage(p, s, 0, in_unit * U);
+        if (rc == FCW_OK) rc = ensure_stage(p, s, 1, out_unit * U);
+    }
+    for (int u0 = 0, c = 0; rc == FCW_OK && u0 < S; u0 += U, ++c) {
+        const int n = std::min(U, S - u0);
+        const int set = c & 1;
+        cudaStream_t st = p->streams[set];
+        cudaError_t e = cudaMemcpyAsync(p->stage[set][0], static_cast<const char*>(grid_host) + in_unit * u0,
+                                        in_unit * n, cudaMemcpyHostToDevice, st);
+        if (e != cudaSuccess) {
+            rc = cuda_fail(e, "H2D");
+            break;
+        }
+        rc = fcw_tx(p, p->stage[set][0], 0, p->stage[set][1], 0, n, flags, st);
+        if (rc) break;
+        e = cudaMemcpyAsync(static_cast<char*>(wave_host) + out_unit * u0, p->stage[set][1], out_unit * n,
+                            cudaMemcpyDeviceToHost, st);
+        if (e != cudaSuccess) rc = cuda_fail(e, "D2H");
+    }
+    for (int s = 0; s < 2; ++s) {
+        const cudaError_t e = cudaStreamSynchronize(p->streams[s]);
+        if (e != cudaSuccess && rc == FCW_OK) rc = cuda_fail(e, "tx_host sync");
+    }
+    cudaSetDevice(cur);
+    return rc;
+}
+
+int fcw_rx_host(fcw_plan* p, const void* wave_host, int64_t wave_len, int64_t useful0, void* grid_host, int S,
+                unsigned flags) {
+    if (!p) return fail(FCW_EINVAL, "null plan");
+    if (S <= 0) return S == 0 ? FCW_OK : fail(FCW_EINVAL, "negative unit count");
+    if (!grid_host || !wave_host) return fail(FCW_EINVAL, "null buffer");
+    std::lock_guard<std::mutex> lk(p->host_mu);
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(p->device);
+    const int row = (flags & FCW_GRID_FULL) ? p->row_full : p->row_active;
+    const size_t in_unit = sizeof(float2) * (size_t)wave_len;
+    const size_t out_unit = sizeof(float2) * (size_t)p->B * row;
+    const int U = units_per_chunk(in_unit, out_unit, S);
+    int rc = ensure_streams(p);
+    for (int s = 0; rc == FCW_OK && s < 2; ++s) {
+        rc = ensure_stage(p, s, 0, in_unit * U);
+        if (rc == FCW_OK) rc = ensure_stage(p, s, 1, out_unit * U);
+    }
+    for (int u0 = 0, c = 0; rc == FCW_OK && u0 < S; u0 += U, ++c) {
+        const int n = std::min(U, S - u0);
+        const int set = c & 1;
+        cudaStream_t st = p->streams[set];
+        cudaError_t e = cudaMemcpyAsync(p->stage[set][0], static_cast<const char*>(wave_host) + in_unit * u0,
+                                        in_unit * n, cudaMemcpyHostToDevice, st);
+        if (e != cudaSuccess) {
+            rc = cuda_fail(e, "H2D");
+            break;
+        }
+        rc = fcw_rx(p, p->stage[set][0], 0, wave_len, useful0, p->stage[set][1], 0, n, flags, st);
+        if (rc) break;
+        e = cudaMemcpyAsync(static_cast<char*>(grid_host) + out_unit * u0, p->stage[set][1], out_unit * n,
+                            cudaMemcpyDeviceToHost, st);
+        if (e != cudaSuccess) rc = cuda_fail(e, "D2H");
+    }
+    for (int s = 0; s < 2; ++s) {
+        const cudaError_t e = cudaStreamSynchronize(p->streams[s]);
+        if (e != cudaSuccess && rc == FCW_OK) rc = cuda_fail(e, "rx_host sync");
+    }
+    cudaSetDevice(cur);
+    return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,236 @@
+// Register / shared-memory FFT building blocks for sm_100a (complex fp32).
+//
+//  * fft_reg<R, SIGN>: natural-order in/out radix-2 DIT transform of R points
+//    held in registers, fully unrolled; its twiddles are compile-time
+//    immediates (constexpr cos/sin evaluated by the front end).
+//  * team_fft<n, T, PPT, SIGN, NF, CTA>: Stockham autosort transform of size
+//    n = T * PPT run by a team of T threads (a warp or the CTA), NF transforms
+//    in lockstep sharing twiddles.  Input and output are in the cyclic
+//    distribution v[m] = x[t + T*m]; intermediate passes go through a padded
+//    shared-memory buffer (one pad slot per 16, bank-conflict free for every
+//    radix used).  Runtime twiddles come from the plan's N-entry table.
+//
+// SIGN = -1: forward (e^{-j}, unscaled) like fft::forward (proj/src/fft.cpp:47-52);
+// SIGN = +1: inverse WITHOUT the 1/n factor (callers fold scales elsewhere).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#define FCW_DI __device__ __forceinline__
+
+namespace fcw {
+
+// ------------------------------------------------------ compile-time trig
+constexpr double cx_pi = 3.14159265358979323846264338327950288;
+
+__host__ __device__ constexpr double cx_sin_small(double x) {
+    double x2 = x * x, term = x, sum = x;
+    for (int i = 1; i < 14; ++i) {
+        term *= -x2 / ((2.0 * i) * (2.0 * i + 1.0));
+        sum += term;
+    }
+    return sum;
+}
+__host__ __device__ constexpr double cx_cos_small(double x) {
+    double x2 = x * x, term = 1.0, sum = 1.0;
+    for (int i = 1; i < 14; ++i) {
+        term *= -x2 / ((2.0 * i - 1.0) * (2.0 * i));
+        sum += term;
+    }
+    return sum;
+}
+// cos(2*pi*f) for a turn fraction f that is exact in binary (k/n, n a power
+// of two), by octant reduction to |angle| <= pi/4.
+__host__ __device__ constexpr double cx_cos_turn(double f) {
+    f = f - (double)(long long)f;
+    if (f < 0) f += 1.0;
+    if (f > 0.5) f = 1.0 - f;                                   // even
+    if (f > 0.25) return -cx_cos_turn(0.5 - f);                 // cos(pi - a) = -cos(a)
+    if (f > 0.125) return cx_sin_small(2.0 * cx_pi * (0.25 - f));  // cos(a) = sin(pi/2 - a)
+    return cx_cos_small(2.0 * cx_pi * f);
+}
+__host__ __device__ constexpr double cx_cos2pi(long k, long n) { return cx_cos_turn((double)k / (double)n); }
+__host__ __device__ constexpr double cx_sin2pi(long k, long n) {
+    return cx_cos_turn((double)k / (double)n - 0.25);  // sin(a) = cos(a - pi/2)
+}
+
+template <int N_, int K_, int SIGN>
+struct Tw {
+    static constexpr float re = (float)cx_cos2pi(K_, N_);
+    static constexpr float im = (float)(SIGN * cx_sin2pi(K_, N_));
+};
+
+// --------------------------------------------------------- complex helpers
+FCW_DI float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+FCW_DI float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+FCW_DI float2 cmul(float2 a, float2 b) {
+    return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+FCW_DI float2 cmulc(float2 a, float2 b) {  // a * conj(b)
+    return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
+}
+FCW_DI float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+FCW_DI float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
+// multiply by j^k (compile-time k)
+template <int K>
+FCW_DI float2 mul_jpow(float2 a) {
+    constexpr int k = ((K % 4) + 4) % 4;
+    if constexpr (k == 0) return a;
+    if constexpr (k == 1) return make_float2(-a.y, a.x);
+    if constexpr (k == 2) return make_float2(-a.x, -a.y);
+    return make_float2(a.y, -a.x);
+}
+FCW_DI float2 mul_jpow_rt(float2 a, int k) {
+    k &= 3;
+    if (k == 0) return a;
+    if (k == 1) return make_float2(-a.y, a.x);
+    if (k == 2) return make_float2(-a.x, -a.y);
+    return make_float2(a.y, -a.x);
+}
+
+__host__ __device__ constexpr int cx_log2(int v) { return v <= 1 ? 0 : 1 + cx_log2(v / 2); }
+__host__ __device__ constexpr int cx_brev(int v, int bits) {
+    int r = 0;
+    for (int i = 0; i < bits; ++i) r |= ((v >> i) & 1) << (bits - 1 - i);
+    return r;
+}
+
+// ----------------------------------------------------- register radix-2 DIT
+template <int L, int SIGN, int LEN, int K>
+FCW_DI void fft_stage(float2 (&x)[L]) {
+    if constexpr (LEN <= L) {
+        if constexpr (K < LEN / 2) {
+            constexpr int H = LEN / 2;
+#pragma unroll
+            for (int s = 0; s < L; s += LEN) {
+                const float2 a = x[s + K];
+                const float2 b = x[s + K + H];
+                float2 wb;
+                if constexpr (K == 0) {
+                    wb = b;
+                } else if constexpr (4 * K == LEN) {
+                    wb = SIGN < 0 ? make_float2(b.y, -b.x) : make_float2(-b.y, b.x);
+                } else {
+                    constexpr float wr = Tw<LEN, K, SIGN>::re;
+                    constexpr float wi = Tw<LEN, K, SIGN>::im;
+                    wb = make_float2(fmaf(b.x, wr, -b.y * wi), fmaf(b.x, wi, b.y * wr));
+                }
+                x[s + K] = cadd(a, wb);
+                x[s + K + H] = csub(a, wb);
+            }
+            fft_stage<L, SIGN, LEN, K + 1>(x);
+        } else {
+            fft_stage<L, SIGN, LEN * 2, 0>(x);
+        }
+    }
+}
+
+template <int L, int SIGN>
+FCW_DI void fft_reg(float2 (&x)[L]) {
+    if constexpr (L == 1) return;
+    constexpr int LB = cx_log2(L);
+#pragma unroll
+    for (int i = 0; i < L; ++i) {
+        const int j = cx_brev(i, LB);
+        if (i < j) {
+            const float2 t = x[i];
+            x[i] = x[j];
+            x[j] = t;
+        }
+    }
+    fft_stage<L, SIGN, 2, 0>(x);
+}
+
+// ------------------------------------------------------------ team barriers
+template <bool CTA>
+FCW_DI void team_bar() {
+    if constexpr (CTA)
+        __syncthreads();
+    else
+        __syncwarp();
+}
+
+FCW_DI int spad(int e) { return e + (e >> 4); }
+
+// One Stockham pass (and the remaining ones, recursively).
+template <int n, int T, int PPT, int SIGN, int NF, bool CTA, int NS>
+FCW_DI void team_pass(float2 (&v)[NF][PPT], float2* const* buf, const float2* __restrict__ tw,
+                      int ts, int t, bool act) {
+    constexpr int R0 = PPT < 16 ? PPT : 16;
+    constexpr int REM = n / NS;
+    constexpr int R = REM < R0 ? REM : R0;
+    constexpr bool LAST = (NS * R == n);
+    constexpr int NB = PPT / R;
+    static_assert(R >= 2 && PPT % R == 0, "team_fft: bad radix schedule");
+    if (act) {
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+            const int j = t + T * i;
+            float2 y[NF][R];
+#pragma unroll
+            for (int f = 0; f < NF; ++f)
+#pragma unroll
+                for (int k = 0; k < R; ++k) y[f][k] = v[f][i + k * NB];
+            if constexpr (NS > 1) {
+                const int jm = j & (NS - 1);
+#pragma unroll
+                for (int k = 1; k < R; ++k) {
+                    const int e = jm * k * (n / (NS * R));
+                    float2 w = __ldg(&tw[e * ts]);
+                    if constexpr (SIGN > 0) w.y = -w.y;
+#pragma unroll
+                    for (int f = 0; f < NF; ++f) y[f][k] = cmul(y[f][k], w);
+                }
+            }
+#pragma unroll
+            for (int f = 0; f < NF; ++f) fft_reg<R, SIGN>(y[f]);
+#pragma unroll
+            for (int f = 0; f < NF; ++f)
+#pragma unroll
+                for (int k = 0; k < R; ++k) v[f][i + k * NB] = y[f][k];
+        }
+    }
+    if constexpr (!LAST) {
+        team_bar<CTA>();
+        if (act) {
+#pragma unroll
+            for (int i = 0; i < NB; ++i) {
+                const int j = t + T * i;
+                const int base = (j / NS) * NS * R + (j & (NS - 1));
+#pragma unroll
+                for (int f = 0; f < NF; ++f)
+#pragma unroll
+                    for (int k = 0; k < R; ++k) buf[f][spad(base + k * NS)] = v[f][i + k * NB];
+            }
+        }
+        team_bar<CTA>();
+        if (act) {
+#pragma unroll
+            for (int f = 0; f < NF; ++f)
+#pragma unroll
+                for (int m = 0; m < PPT; ++m) v[f][m] = buf[f][spad(t + T * m)];
+        }
+        team_pass<n, T, PPT, SIGN, NF, CTA, NS * R>(v, buf, tw, ts, t, act);
+    }
+}
+
+// Full transform.  All T threads of the team (and, for CTA teams, every
+// thread of the block) must call it; threads with act == false only join the
+// barriers.  The buffers must hold spad(n) + 1 float2 each and may alias the
+// input's source memory once it has been read into v.
+template <int n, int T, int PPT, int SIGN, int NF, bool CTA>
+FCW_DI void team_fft(float2 (&v)[NF][PPT], float2* const* buf, const float2* __restrict__ tw, int ts,
+                     int t, bool act) {
+    static_assert(n == T * PPT, "team_fft: n != T*PPT");
+    if constexpr (n == 1) return;
+    if constexpr (T == 1) {
+        if (act) {
+#pragma unroll
+            for (int f = 0; f < NF; ++f) fft_reg<PPT, SIGN>(v[f]);
+        }
+    } else {
+        team_pass<n, T, PPT, SIGN, NF, CTA, 1>(v, buf, tw, ts, t, act);
+    }
+}
+
+}  // namespace fcw

@@ -1,0 +1,126 @@
+// Internal definitions shared by the host plan builder and the sm_100a
+// kernels.  Not part of the public ABI (include/fcwave_b200.h is).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "fcwave_b200.h"
+
+namespace fcw {
+
+constexpr int kThreads = 256;     // CTA size of both kernels
+constexpr int kWarps = kThreads / 32;
+constexpr int kMaxN = 4096;       // long transform envelope (SMEM-resident blocks)
+constexpr int kMaxL = 1024;       // short transform envelope (warp-resident)
+constexpr int kMaxGroups = 9;     // distinct L values: 4..1024
+constexpr int kMaxLevels = 8;     // contributor ranks per shared bin
+
+// Per-subband constants resident in HBM (read through L1).
+struct SubDev {
+    int L, logL, c, logI;
+    int act_off;   // offset of this subband's active bins in a packed grid row
+    int n_act;
+    int full_off;  // offset of this subband's L bins in a full grid row / table row
+    int cmodN;     // c mod N (for the symbol rotator exponent)
+    float bp1;     // block_phase(1, c, L/2, L) = +-1 (fc_core.cpp:41-44, lambda = 1/2)
+    float tx_scale;  // sqrt(I) / (N sqrt(L)): folds ofdm_modulate sqrt(L)/L, IDFT_N 1/N, tx_symbol sqrt(I)
+    float rx_s0;     // sqrt(I) (L/N) / sqrt(L)  (fc_sync.cpp:238-240)
+    float pad_;
+};
+
+// Per-symbol geometry (all integer-exact on the host).
+struct SymDev {
+    long long sigma;  // symbol_sigma (fc_sync.cpp:86-88)
+    int cp;           // N_CP,n
+    int own_len;      // samples [sigma_n, sigma_n+own_len) owned by symbol n's tile
+    int carry_len;    // leading samples that also receive the previous symbol's block 1
+    int smodN;        // (sum_{q=1..n} N_CP,q) mod N
+    int pad_[2];
+};
+
+// Kernel parameter block (passed by value).
+struct KParams {
+    int N, B, M;
+    int chunk, nchunks;
+    int spec_stride;  // float2 per block spectrum in SMEM (>= N + n_ext, >= N + N/16)
+    int scratch_stride;  // float2 per warp scratch
+    int row_len;
+    int grid_full;
+    int fused;
+    int n_ext, n_zero, n_lvl;
+    int lvl_start[kMaxLevels + 1];
+    int n_groups;
+    int grp_L[kMaxGroups], grp_start[kMaxGroups], grp_count[kMaxGroups];
+    long long Q;
+    long long rx_base;   // useful0 - N_L
+    long long wave_len;
+    long long in_stride, out_stride;
+    const SubDev* sub;
+    const SymDev* sym;
+    const float* win;    // [sum L] shifted-domain window per subband
+    const int* inv;      // [sum L] DFT bin -> active index or -1
+    const int* dest;     // [sum L] shifted index p0 -> spectrum slot (q or N + ext) or -1
+    const int* grp_sub;  // subband ids grouped by L
+    const int* fix_tgt;  // [n_ext] target bin of each secondary contribution
+    const int* zero_list;  // [n_zero] bins no subband touches
+    const float2* tw;    // [N] exp(-2 pi i k / N)
+    const float2* in;
+    float2* out;
+};
+
+struct Plan {
+    int device = 0;
+    int N = 0, B = 0, M = 0;
+    double overlap = 0.5;
+    fcw_fc_params pN{};  // N-side geometry (N_L, N_T shared by all subbands)
+    long long Q = 0, useful0 = 0, frame_samples = 0;
+    int row_active = 0, row_full = 0;
+    int chunk = 0;
+    std::vector<int> cp;
+    std::vector<long long> sigma;
+    struct Sub {
+        fcw_subband desc;
+        std::vector<int> bins;
+        std::vector<double> window;
+        fcw_fc_params p;
+    };
+    std::vector<Sub> subs;
+    // host images of the device tables
+    std::vector<SubDev> h_sub;
+    std::vector<SymDev> h_sym;
+    std::vector<float> h_win;
+    std::vector<int> h_inv, h_dest, h_grp_sub, h_fix, h_zero;
+    int n_ext = 0, n_lvl = 0;
+    std::vector<int> lvl_start;
+    int n_groups = 0;
+    int grp_L[kMaxGroups]{}, grp_start[kMaxGroups]{}, grp_count[kMaxGroups]{};
+    int Lmax = 0;
+    // device tables (one allocation)
+    void* d_blob = nullptr;
+    SubDev* d_sub = nullptr;
+    SymDev* d_sym = nullptr;
+    float* d_win = nullptr;
+    int *d_inv = nullptr, *d_dest = nullptr, *d_grp_sub = nullptr, *d_fix = nullptr, *d_zero = nullptr;
+    float2* d_tw = nullptr;
+    // host-buffer pipeline state
+    std::mutex host_mu;
+    cudaStream_t streams[2] = {nullptr, nullptr};
+    void* stage[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+    size_t stage_bytes[2][2] = {{0, 0}, {0, 0}};
+};
+
+// kernels.cu
+cudaError_t launch_tx(const Plan& plan, KParams& kp, int S, cudaStream_t st);
+cudaError_t launch_rx(const Plan& plan, KParams& kp, int S, cudaStream_t st);
+cudaError_t launch_gen_qam(const Plan& plan, uint64_t seed, long long unit0, int S, int bits,
+                           float2* out, cudaStream_t st);
+size_t tx_smem_bytes(const Plan& plan);
+size_t rx_smem_bytes(const Plan& plan);
+void fill_common(const Plan& plan, KParams& kp);
+
+}  // namespace fcw
