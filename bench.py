@@ -1,0 +1,359 @@
+#!/usr/bin/env python3
+"""FC-F-OFDM TX+RX throughput on B200 (BASELINE.json metric).
+
+One step = TX synthesis of every local unit (antenna stream x frame) from its
+device-resident packed QAM grid, followed by fused RX analysis of every local
+unit from the TX waveform.  value = air-interface samples sum_n (N + N_CP,n)
+of all units on all ranks / max-over-ranks device time.
+
+  python bench.py [--config c5] [--gpus N --steps K --warmup W] [--impl reference]
+
+Multi-GPU: launched by torchrun, one rank per GPU; units are sharded by
+(stream, frame) with no data-path collective; the only
+collectives are the barrier around the timed region and the max-reduce of the
+elapsed time after it.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "FC-F-OFDM TX+RX Msamples/s per GPU and at 8 GPUs; % of HBM roofline"
+UNIT = "Msamples/s"
+SEED = 20080672
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c5", choices=["c1", "c2", "c4", "c5"])
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--rx", default="fused", choices=["fused", "direct"])
+    ap.add_argument("--units", type=int, default=0, help="override total units (default: the config's)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def shard(total: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous block of units for `rank` (first total % world ranks get one more)."""
+    base, rem = divmod(total, world)
+    lo = rank * base + min(rank, rem)
+    return lo, base + (1 if rank < rem else 0)
+
+
+def hbm_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "50", "-i", str(self.idx)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.12)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons, power = [], None, set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+                power.append(float(parts[3]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm),
+                "power_w_max": max(power) if power else None}
+
+
+# ------------------------------------------------------------------ CPU legs
+def cpu_reference(w, units: int, threads: int, fused: bool, steps: int = 1):
+    """The reference's own path (oracle/_ref = unmodified fcwave + FFTW shim) on
+    `threads` host threads over `units` whole stream-frames.  Returns
+    (Msamples/s per step list, kind, sample description)."""
+    import oracle as O
+
+    plan_rows = sum(len(b) for b in w.active_maps)
+    packed = O.gen_grid(SEED, 0, units, w.B, plan_rows, w.bits_per_symbol).astype(np.complex64)
+    vals = []
+    if O.ref_available():
+        kind = "reference"
+        for _ in range(steps):
+            t, _chk = O.Ref.bench_txrx(w.N, w.cp, [s.L for s in w.subbands], [s.c for s in w.subbands],
+                                       [s.window for s in w.subbands], [len(b) for b in w.active_maps],
+                                       w.active_maps, packed, units, threads, simplified=fused)
+            vals.append(units * sum(w.N + c for c in w.cp) / t / 1e6)
+    else:
+        kind = "port"
+        from concurrent.futures import ThreadPoolExecutor
+
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        from helpers import oracle_rx, oracle_tx
+
+        def one(u):
+            wv, u0 = oracle_tx(w, packed[u].astype(np.complex128))
+            oracle_rx(w, wv, u0, fused)
+
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            with ThreadPoolExecutor(threads) as ex:
+                list(ex.map(one, range(units)))
+            vals.append(units * sum(w.N + c for c in w.cp) / (time.perf_counter() - t0) / 1e6)
+    sample = (f"{units} whole {w.name} units (B={w.B} symbols, {len(w.subbands)} subbands each): "
+              f"tx_discontinuous over all subbands + rx_discontinuous per subband "
+              f"({'fused' if fused else 'direct'}), one unit per thread; FFT via builder-written FFTW-API shim "
+              f"(FFTW3 absent; an FFTW-backed reference would be faster)")
+    return vals, kind, sample
+
+
+def cpu_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference_arm(args, w):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    threads = cpu_threads()
+    units = max(1, min(threads, w.units))
+    if w.name.startswith("c1"):
+        units = max(units, 256)
+    vals, kind, sample = cpu_reference(w, units, threads, args.rx == "fused", steps=args.warmup + args.steps)
+    timed = vals[args.warmup:] if len(vals) > args.warmup else vals
+    value = statistics.mean(timed)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": w.name, "units_sampled": units, "description": w.description},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU arm
+def main():
+    args = parse()
+    from paper_2008_00672_b200 import configs
+
+    w = configs.get(args.config)
+    if args.units:
+        w.units = args.units
+    if args.impl == "reference":
+        run_reference_arm(args, w)
+        return
+
+    import torch
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    plan = w.plan()
+    u0, S = shard(w.units, rank, world)
+    fused = args.rx == "fused"
+    dev = torch.device("cuda", local)
+    grid = torch.empty((S, w.B, plan.row_active), dtype=torch.complex64, device=dev)
+    wave = torch.empty((S, plan.Q), dtype=torch.complex64, device=dev)
+    out = torch.empty_like(grid)
+    plan.gen_qam(SEED, u0, S, w.bits_per_symbol, grid)
+    stream = torch.cuda.current_stream()
+
+    def step(ev=None):
+        if ev:
+            ev[0].record(stream)
+        plan.tx(grid, wave, S, stream=stream)
+        if ev:
+            ev[1].record(stream)
+        plan.rx(wave, plan.Q, plan.useful0, out, S, fused=fused, stream=stream)
+        if ev:
+            ev[2].record(stream)
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    clk = ClockSampler(local) if rank == 0 else None
+    if clk:
+        clk.start()
+        time.sleep(0.15)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for k in range(args.steps):
+        step(evs[k])
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clocks = clk.stop() if clk else None
+    elapsed_ms = t_start.elapsed_time(t_end)
+    tx_ms = [e[0].elapsed_time(e[1]) for e in evs]
+    rx_ms = [e[1].elapsed_time(e[2]) for e in evs]
+    stats = torch.tensor([elapsed_ms, statistics.mean(tx_ms), statistics.mean(rx_ms)], dtype=torch.float64,
+                         device=dev)
+    if dist:
+        dist.all_reduce(stats, op=dist.ReduceOp.MAX)
+    elapsed_ms, tx_avg, rx_avg = [float(x) for x in stats.tolist()]
+    ms_per_step = elapsed_ms / args.steps
+    total_samples = w.units * plan.frame_samples
+    value = total_samples / (ms_per_step * 1e-3) / 1e6
+
+    # roofline of the dominant kernel (algorithmic bytes per launch / mean launch time)
+    ab = configs.algorithmic_bytes_per_unit(w, plan.row_active, plan.Q)
+    peak, peak_src = hbm_peak()
+    dom = "rx" if rx_avg > tx_avg else "tx"
+    dom_ms = max(rx_avg, tx_avg)
+    achieved = ab[dom] * S / (dom_ms * 1e-3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as f:
+                tj = json.load(f)
+            t_ent = tj.get(w.name, {}).get(dom)
+            if t_ent:
+                traffic = t_ent.get("dram_bytes_per_unit", 0) * S
+        except Exception:
+            traffic = None
+    both_gbs = ab["total"] * S / (ms_per_step * 1e-3) / 1e9
+
+    # e2e through the host-buffer C ABI (pinned host memory, copies in the timed region)
+    e2e = None
+    if not args.no_e2e:
+        from paper_2008_00672_b200 import PinnedBuffer
+
+        del out
+        torch.cuda.empty_cache()
+        hg = PinnedBuffer((S, w.B, plan.row_active))
+        hw = PinnedBuffer((S, plan.Q))
+        ho = PinnedBuffer((S, w.B, plan.row_active))
+        hg.array[...] = grid.cpu().numpy()
+        del grid, wave
+        torch.cuda.empty_cache()
+        plan.tx_host(hg.array, S, out=hw.array)  # warm (staging buffers, streams)
+        plan.rx_host(hw.array, plan.Q, plan.useful0, S, fused=fused, out=ho.array)
+        n_e2e = max(1, args.e2e_steps)
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(n_e2e):
+            plan.tx_host(hg.array, S, out=hw.array)
+            plan.rx_host(hw.array, plan.Q, plan.useful0, S, fused=fused, out=ho.array)
+        e2e_s = time.perf_counter() - t0
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        if dist:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item()) / n_e2e
+        grid_b = 8 * w.B * plan.row_active * w.units
+        wave_b = 8 * plan.Q * w.units
+        e2e = {"value": total_samples / e2e_s / 1e6, "unit": UNIT, "h2d_bytes_per_step": grid_b + wave_b,
+               "d2h_bytes_per_step": wave_b + grid_b, "steps": n_e2e,
+               "path": "fcw_tx_host + fcw_rx_host (pinned host buffers, 2-stream H2D/kernel/D2H pipeline)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        threads = cpu_threads()
+        units = max(1, min(threads, w.units))
+        vals, kind, sample = cpu_reference(w, units, threads, fused, steps=1)
+        cpu = {"value": vals[0], "unit": UNIT, "cores": threads, "kind": kind, "sample": sample}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": w.name, "units": w.units, "units_per_gpu": S, "symbols_per_unit": w.B,
+                       "subbands": len(w.subbands), "N": w.N, "rx_path": args.rx,
+                       "l2": "inputs larger than L2 (working set %.1f GB)" % (ab["total"] * w.units / 2 / 1e9),
+                       "description": w.description},
+            "roofline": {"bound": "hbm", "kernel": f"{dom}_kernel<{w.N}>", "achieved": achieved, "peak": peak,
+                         "unit": "GB/s", "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "algorithmic_bytes_per_unit": ab[dom],
+                         "txrx_achieved_gbs": both_gbs, "txrx_frac": both_gbs / peak},
+            "kernels_ms": {"tx": tx_avg, "rx": rx_avg},
+            "gpu_launches": 2 * args.steps,
+            "clocks": clocks,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -81,6 +81,8 @@ def lib():
             f.restype = None
         L.fco_symbol_phase.argtypes = [C.c_int, C.c_int, _i32p, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]
         L.fco_symbol_phase.restype = None
+        L.fco_zero_pad_symbol.argtypes = [_f64p, C.c_int, C.POINTER(FcoParams), C.c_int, _f64p]
+        L.fco_first_block_window.argtypes = [C.POINTER(FcoParams), C.c_int, _f64p]
         L.fco_fft.argtypes = [_f64p, C.c_int, C.c_int]
         L.fco_fft.restype = None
         L.fco_tx_symbol.argtypes = [_f64p, C.c_int, C.c_int, C.c_int, _f64p, C.POINTER(FcoParams), _i32p, C.c_int, _f64p]
@@ -228,6 +230,21 @@ def symbol_phase(n: int, c: int, cp, N: int) -> complex:
     a, b = C.c_double(), C.c_double()
     lib().fco_symbol_phase(n, c, _i32(cp), N, C.byref(a), C.byref(b))
     return complex(a.value, b.value)
+
+
+def zero_pad_symbol(sym, p: Params, l_cp: int) -> np.ndarray:
+    s = _as_f64(sym)
+    out = np.zeros(2 * (3 * p.L // 2), np.float64)
+    pc = p.c()
+    _check(lib().fco_zero_pad_symbol(s, len(s) // 2, C.byref(pc), l_cp, out), "zero_pad_symbol")
+    return out.view(np.complex128)
+
+
+def first_block_window(p: Params, l_cp: int) -> np.ndarray:
+    a = np.zeros(p.L, np.float64)
+    pc = p.c()
+    _check(lib().fco_first_block_window(C.byref(pc), l_cp, a), "first_block_window")
+    return a
 
 
 def fft(x, inverse: bool = False) -> np.ndarray:

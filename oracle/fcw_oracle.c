@@ -124,6 +124,24 @@ void fco_symbol_phase(int n, int c, const int* cp, int N, double* re, double* im
     *im = sin(a);
 }
 
+/* fc_sync.cpp:34-43 */
+int fco_zero_pad_symbol(const double* sym, int sym_len, const fco_params* p, int l_cp, double* z) {
+    if (l_cp > p->L_L) return 1;
+    if (sym_len != p->L + l_cp) return 1;
+    const int s_l = p->L_L - l_cp;
+    memset(z, 0, sizeof(double) * 2 * (size_t)(3 * p->L / 2));
+    memcpy(z + 2 * s_l, sym, sizeof(double) * 2 * (size_t)sym_len);
+    return 0;
+}
+
+/* fc_sync.cpp:52-58: passes [S_L, S_L + L_S + l_cp) */
+int fco_first_block_window(const fco_params* p, int l_cp, double* a) {
+    if (l_cp > p->L_L) return 1;
+    const int s_l = p->L_L - l_cp;
+    for (int i = 0; i < p->L; ++i) a[i] = (i >= s_l && i < s_l + p->L_S + l_cp) ? 1.0 : 0.0;
+    return 0;
+}
+
 /* DFT definition of proj/src/fft.cpp:47-61 (FFTW forward/backward). */
 void fco_fft(double* d, int n, int inverse) {
     if (n <= 1) return;

@@ -45,6 +45,10 @@ int fco_centered_active_map(int l_ofdm, int n_active, int skip_dc, int* bins);
 void fco_block_phase(int64_t r, int c, int L_S, int L, double* re, double* im);
 void fco_symbol_phase(int n, int c, const int* cp, int N, double* re, double* im);
 
+/* fc_sync.cpp:34-43 (z length 3L/2) and :52-58 (first-block window) */
+int fco_zero_pad_symbol(const double* sym, int sym_len, const fco_params* p, int l_cp, double* z);
+int fco_first_block_window(const fco_params* p, int l_cp, double* a);
+
 /* In-place DFT: forward unscaled e^{-j}; inverse e^{+j} with 1/n. */
 void fco_fft(double* data, int n, int inverse);
 
