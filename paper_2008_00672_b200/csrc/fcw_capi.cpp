@@ -355,6 +355,22 @@ int fcw_plan_create(fcw_plan** out, int N, double overlap, const int* cp_high, i
         s.smodN = (int)mod_ll(cp_partial(p->cp, n), N);
         p->h_sym[n] = s;
     }
+    // packed per-bin table, indexed by DFT bin b (p0 = b ^ L/2)
+    p->h_bin.resize(p->h_inv.size());
+    for (int m = 0; m < M; ++m) {
+        const fcw::SubDev& d = p->h_sub[m];
+        for (int b = 0; b < d.L; ++b) {
+            const int p0 = b ^ (d.L / 2);
+            const float w = p->h_win[d.full_off + p0];
+            const float w1 = w * d.bp1;
+            int4 e;
+            e.x = p->h_inv[d.full_off + b];
+            e.y = p->h_dest[d.full_off + p0];
+            std::memcpy(&e.z, &w, 4);
+            std::memcpy(&e.w, &w1, 4);
+            p->h_bin[d.full_off + b] = e;
+        }
+    }
     // device tables in one blob
     std::vector<float2> tw(N);
     for (int k = 0; k < N; ++k) {
@@ -367,12 +383,10 @@ int fcw_plan_create(fcw_plan** out, int N, double overlap, const int* cp_high, i
     off = align(off + sizeof(fcw::SubDev) * M);
     const size_t o_sym = off;
     off = align(off + sizeof(fcw::SymDev) * B);
-    const size_t o_win = off;
-    off = align(off + sizeof(float) * p->h_win.size());
+    const size_t o_bin = off;
+    off = align(off + sizeof(int4) * p->h_bin.size());
     const size_t o_inv = off;
     off = align(off + sizeof(int) * p->h_inv.size());
-    const size_t o_dest = off;
-    off = align(off + sizeof(int) * p->h_dest.size());
     const size_t o_grp = off;
     off = align(off + sizeof(int) * p->h_grp_sub.size());
     const size_t o_fix = off;
@@ -384,9 +398,8 @@ int fcw_plan_create(fcw_plan** out, int N, double overlap, const int* cp_high, i
     std::vector<unsigned char> host(off, 0);
     std::memcpy(&host[o_sub], p->h_sub.data(), sizeof(fcw::SubDev) * M);
     std::memcpy(&host[o_sym], p->h_sym.data(), sizeof(fcw::SymDev) * B);
-    std::memcpy(&host[o_win], p->h_win.data(), sizeof(float) * p->h_win.size());
+    std::memcpy(&host[o_bin], p->h_bin.data(), sizeof(int4) * p->h_bin.size());
     std::memcpy(&host[o_inv], p->h_inv.data(), sizeof(int) * p->h_inv.size());
-    std::memcpy(&host[o_dest], p->h_dest.data(), sizeof(int) * p->h_dest.size());
     std::memcpy(&host[o_grp], p->h_grp_sub.data(), sizeof(int) * p->h_grp_sub.size());
     if (!p->h_fix.empty()) std::memcpy(&host[o_fix], p->h_fix.data(), sizeof(int) * p->h_fix.size());
     if (!p->h_zero.empty()) std::memcpy(&host[o_zero], p->h_zero.data(), sizeof(int) * p->h_zero.size());
@@ -405,9 +418,8 @@ int fcw_plan_create(fcw_plan** out, int N, double overlap, const int* cp_high, i
     auto* base = static_cast<unsigned char*>(p->d_blob);
     p->d_sub = reinterpret_cast<fcw::SubDev*>(base + o_sub);
     p->d_sym = reinterpret_cast<fcw::SymDev*>(base + o_sym);
-    p->d_win = reinterpret_cast<float*>(base + o_win);
+    p->d_bin = reinterpret_cast<int4*>(base + o_bin);
     p->d_inv = reinterpret_cast<int*>(base + o_inv);
-    p->d_dest = reinterpret_cast<int*>(base + o_dest);
     p->d_grp_sub = reinterpret_cast<int*>(base + o_grp);
     p->d_fix = reinterpret_cast<int*>(base + o_fix);
     p->d_zero = reinterpret_cast<int*>(base + o_zero);

@@ -1,0 +1,514 @@
+// sm_100a kernels of the symbol-synchronized FC-F-OFDM hot path (templates;
+// instantiated per long-transform size N in fcw_k_*.cu).
+//
+//  K-TX  tx_kernel<N, LU>: fused TX synthesis (replaces tx_discontinuous,
+//        proj/src/fc_sync.cpp:114-143 and everything under it:
+//        ofdm_modulate ofdm.cpp:97, cp_insert :108, zero_pad_symbol
+//        fc_sync.cpp:34, tx_symbol :60, sfb_block_ola/synth_core
+//        fc_core.cpp:115,76, combine_symbols fc_sync.cpp:96, subband sum :139).
+//  K-RX  rx_kernel<N, LU>: fused RX analysis for all subbands (replaces
+//        rx_discontinuous fc_sync.cpp:245 with rx_segment :145, rx_block_freq
+//        :178, rx_symbol_simplified :195 / rx_symbol_direct :158 +
+//        afb_block_ols fc_core.cpp:144 + ofdm_demodulate ofdm.cpp:125).
+//  LU = the plan's uniform short-transform size (specialised, 2 CTAs/SM), or
+//  0 for plans mixing several L (generic: one branch per L group).
+//
+// Work decomposition: one CTA (256 threads) owns a run of `chunk` consecutive
+// OFDM symbols of one unit (antenna stream x frame) and walks them in order.
+// Per symbol it builds the two N-bin block spectra of ALL subbands in SMEM
+// (one shared N-point transform per block — the reference runs one per
+// subband), transforms both blocks in lockstep, and overlap-adds in
+// registers.  The tail of block 1 that overlaps the next symbol is carried in
+// SMEM; the CTA recomputes the symbol just before its run to obtain the
+// incoming carry, so every waveform sample is written exactly once by exactly
+// one CTA (no atomics, no zero-fill pass, deterministic).
+#pragma once
+
+#include "fcw_fft.cuh"
+#include "fcw_internal.hpp"
+
+namespace fcw {
+
+constexpr int kPPT = 16;  // long-transform points per thread and block
+
+// Bin-table entry (plan, per subband and DFT bin b):
+//   x = inv[b] (active index of bin b or -1), y = dest[p0(b)] (spectrum slot or -1),
+//   z = bits(w[p0(b)]), w = bits(w[p0(b)] * bp1), with p0(b) = b ^ L/2.
+FCW_DI int4 bin_entry(const KParams& P, const SubDev& sd, int b) { return __ldg(&P.bin[sd.full_off + b]); }
+
+FCW_DI float2 tw_conj(const float2* __restrict__ tw, int e) {
+    const float2 w = __ldg(&tw[e]);
+    return make_float2(w.x, -w.y);
+}
+
+// theta_n exponent: ((c mod N) * (S_n mod N)) mod N   (fc_sync.cpp:45-50)
+template <int N>
+FCW_DI int theta_exp(int cmodN, int smodN) {
+    return (int)(((unsigned)cmodN * (unsigned)smodN) & (unsigned)(N - 1));
+}
+
+FCW_DI float2 zero2() { return make_float2(0.f, 0.f); }
+
+FCW_DI float2 grid_val(const KParams& P, const SubDev& sd, const float2* __restrict__ row, int b, int inv) {
+    if (P.grid_full) return row[sd.full_off + b];
+    return inv >= 0 ? row[sd.act_off + inv] : zero2();
+}
+
+// ---------------------------------------------------------------- K-TX parts
+
+// Short-side TX of one subband-symbol by one thread (L <= 32).
+template <int N, int L>
+FCW_DI void tx_short_thread(const KParams& P, const SymDev& sy, const float2* __restrict__ row,
+                            float2* spec0, float2* spec1, int gstart, int gcount) {
+    for (int i = threadIdx.x; i < gcount; i += kThreads) {
+        const int m = P.grp_sub ? __ldg(&P.grp_sub[gstart + i]) : gstart + i;
+        const SubDev sd = P.sub[m];
+        float2 x[L];
+        const float2 ph = cscale(tw_conj(P.tw, theta_exp<N>(sd.cmodN, sy.smodN)), sd.tx_scale);
+#pragma unroll
+        for (int b = 0; b < L; ++b) x[b] = cmul(grid_val(P, sd, row, b, __ldg(&P.inv[sd.full_off + b])), ph);
+        fft_reg<L, +1>(x);  // ofdm_modulate (scale folded into ph)
+        const int lcp = sy.cp >> sd.logI;  // cp_truncate (fc_sync.cpp:26-32)
+        float2 u0[L], u1[L];
+#pragma unroll
+        for (int k = 0; k < L; ++k) {
+            // block 0: CP + first half through the reduced-overlap window a0;
+            // block 1: second half through a1 (fc_sync.cpp:34-84)
+            const bool in0 = (k >= L / 4 - lcp) && (k < 3 * L / 4);
+            u0[k] = in0 ? x[(k - L / 4) & (L - 1)] : zero2();
+            u1[k] = (k >= L / 4 && k < 3 * L / 4) ? x[(k + L / 4) & (L - 1)] : zero2();
+        }
+        fft_reg<L, -1>(u0);
+        fft_reg<L, -1>(u1);
+#pragma unroll
+        for (int b = 0; b < L; ++b) {
+            const int4 e = bin_entry(P, sd, b);
+            if (e.y >= 0) {
+                spec0[e.y] = cscale(u0[b], __int_as_float(e.z));
+                spec1[e.y] = cscale(u1[b], __int_as_float(e.w));
+            }
+        }
+    }
+}
+
+// Short-side TX of one subband-symbol by one warp (L >= 64), lane holds bins
+// lane + 32k.  One padded scratch buffer per warp.
+template <int N, int L>
+FCW_DI void tx_short_warp(const KParams& P, const SymDev& sy, const float2* __restrict__ row,
+                          float2* spec0, float2* spec1, float2* scr, int gstart, int gcount) {
+    constexpr int PPT = L / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    float2* const b1[1] = {scr};
+    for (int i = warp; i < gcount; i += kWarps) {
+        const int m = P.grp_sub ? __ldg(&P.grp_sub[gstart + i]) : gstart + i;
+        const SubDev sd = P.sub[m];
+        const float2 ph = cscale(tw_conj(P.tw, theta_exp<N>(sd.cmodN, sy.smodN)), sd.tx_scale);
+        int4 ent[PPT];
+        float2 v[1][PPT];
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) {
+            ent[k] = bin_entry(P, sd, lane + 32 * k);
+            v[0][k] = cmul(grid_val(P, sd, row, lane + 32 * k, ent[k].x), ph);
+        }
+        team_fft<L, 32, PPT, +1, 1, false>(v, b1, P.tw, N / L, lane, true);
+        const int lcp = sy.cp >> sd.logI;
+        float2 u0[1][PPT], u1[1][PPT];
+        if constexpr (L >= 128) {
+            // L/4 is a multiple of 32: the circular shifts are register renames
+#pragma unroll
+            for (int k = 0; k < PPT; ++k) {
+                const int e = lane + 32 * k;
+                const bool in0 = (e >= L / 4 - lcp) && (e < 3 * L / 4);
+                const bool in1 = (e >= L / 4) && (e < 3 * L / 4);
+                u0[0][k] = in0 ? v[0][(k - PPT / 4 + PPT) % PPT] : zero2();
+                u1[0][k] = in1 ? v[0][(k + PPT / 4) % PPT] : zero2();
+            }
+        } else {
+            __syncwarp();
+#pragma unroll
+            for (int k = 0; k < PPT; ++k) scr[lane + 32 * k] = v[0][k];
+            __syncwarp();
+#pragma unroll
+            for (int k = 0; k < PPT; ++k) {
+                const int e = lane + 32 * k;
+                const bool in0 = (e >= L / 4 - lcp) && (e < 3 * L / 4);
+                const bool in1 = (e >= L / 4) && (e < 3 * L / 4);
+                u0[0][k] = in0 ? scr[(e - L / 4) & (L - 1)] : zero2();
+                u1[0][k] = in1 ? scr[(e + L / 4) & (L - 1)] : zero2();
+            }
+        }
+        team_fft<L, 32, PPT, -1, 1, false>(u0, b1, P.tw, N / L, lane, true);
+#pragma unroll
+        for (int k = 0; k < PPT; ++k)
+            if (ent[k].y >= 0) spec0[ent[k].y] = cscale(u0[0][k], __int_as_float(ent[k].z));
+        team_fft<L, 32, PPT, -1, 1, false>(u1, b1, P.tw, N / L, lane, true);
+#pragma unroll
+        for (int k = 0; k < PPT; ++k)
+            if (ent[k].y >= 0) spec1[ent[k].y] = cscale(u1[0][k], __int_as_float(ent[k].w));
+    }
+}
+
+template <int N, int L>
+FCW_DI void tx_short_one(const KParams& P, const SymDev& sy, const float2* __restrict__ row, float2* spec0,
+                         float2* spec1, float2* scr, int gs, int gc) {
+    if constexpr (L <= N) {
+        if constexpr (L <= 32)
+            tx_short_thread<N, L>(P, sy, row, spec0, spec1, gs, gc);
+        else
+            tx_short_warp<N, L>(P, sy, row, spec0, spec1, scr, gs, gc);
+    }
+}
+
+template <int N, int LU>
+FCW_DI void tx_short_all(const KParams& P, const SymDev& sy, const float2* __restrict__ row, float2* spec0,
+                         float2* spec1, float2* scr) {
+    if constexpr (LU > 0) {
+        tx_short_one<N, LU>(P, sy, row, spec0, spec1, scr, 0, P.M);
+    } else {
+        for (int g = 0; g < P.n_groups; ++g) {
+            const int gs = P.grp_start[g], gc = P.grp_count[g];
+            switch (P.grp_L[g]) {
+                case 4: tx_short_one<N, 4>(P, sy, row, spec0, spec1, scr, gs, gc); break;
+                case 8: tx_short_one<N, 8>(P, sy, row, spec0, spec1, scr, gs, gc); break;
+                case 16: tx_short_one<N, 16>(P, sy, row, spec0, spec1, scr, gs, gc); break;
+                case 32: tx_short_one<N, 32>(P, sy, row, spec0, spec1, scr, gs, gc); break;
+                case 64: tx_short_one<N, 64>(P, sy, row, spec0, spec1, scr, gs, gc); break;
+                case 128: tx_short_one<N, 128>(P, sy, row, spec0, spec1, scr, gs, gc); break;
+                case 256: tx_short_one<N, 256>(P, sy, row, spec0, spec1, scr, gs, gc); break;
+                case 512: tx_short_one<N, 512>(P, sy, row, spec0, spec1, scr, gs, gc); break;
+                case 1024: tx_short_one<N, 1024>(P, sy, row, spec0, spec1, scr, gs, gc); break;
+                default: break;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------- K-RX parts
+
+template <int N, int L>
+FCW_DI void rx_short_thread(const KParams& P, const SymDev& sy, const float2* spec0, const float2* spec1,
+                            float2* __restrict__ orow, int gstart, int gcount) {
+    for (int i = threadIdx.x; i < gcount; i += kThreads) {
+        const int m = P.grp_sub ? __ldg(&P.grp_sub[gstart + i]) : gstart + i;
+        const SubDev sd = P.sub[m];
+        // rx_block_freq (fc_sync.cpp:178-193) without the per-symbol rotator,
+        // which is applied once at the output (linearity)
+        float2 g0[L], g1[L];
+#pragma unroll
+        for (int b = 0; b < L; ++b) {
+            const int4 e = bin_entry(P, sd, b);
+            const int q = (sd.c - L / 2 + (b ^ (L / 2))) & (N - 1);
+            g0[b] = cscale(spec0[q], __int_as_float(e.z));
+            g1[b] = cscale(spec1[q], __int_as_float(e.w));
+        }
+        const float2 ph = __ldg(&P.tw[theta_exp<N>(sd.cmodN, sy.smodN)]);  // conj(theta_n)
+        if (P.fused) {
+            // Eq. (30): t = Omega_{L/2} g1, f = Omega_{-L/4}(g0 - t), IDFT, S-hat,
+            // DFT, Omega_{L/4}, + t, Omega_{-L/4}  (fc_sync.cpp:195-243)
+#pragma unroll
+            for (int b = 0; b < L; ++b) {
+                if (b & 1) g1[b] = make_float2(-g1[b].x, -g1[b].y);  // t
+                const float2 f = csub(g0[b], g1[b]);
+                switch (b & 3) {
+                    case 0: g0[b] = f; break;
+                    case 1: g0[b] = mul_jpow<1>(f); break;
+                    case 2: g0[b] = mul_jpow<2>(f); break;
+                    default: g0[b] = mul_jpow<3>(f); break;
+                }
+            }
+            fft_reg<L, +1>(g0);
+#pragma unroll
+            for (int k = L / 2; k < L; ++k) g0[k] = zero2();
+            fft_reg<L, -1>(g0);
+            const float a = sd.rx_s0 / (float)L, s = sd.rx_s0;
+#pragma unroll
+            for (int b = 0; b < L; ++b) {
+                float2 tj = g1[b];
+                switch (b & 3) {
+                    case 1: tj = mul_jpow<1>(tj); break;
+                    case 2: tj = mul_jpow<2>(tj); break;
+                    case 3: tj = mul_jpow<3>(tj); break;
+                    default: break;
+                }
+                g0[b] = cmul(make_float2(fmaf(g0[b].x, a, tj.x * s), fmaf(g0[b].y, a, tj.y * s)), ph);
+            }
+        } else {
+            // direct path: two OLS analysis blocks, central halves, OFDM DFT
+            fft_reg<L, +1>(g0);
+            fft_reg<L, +1>(g1);
+            float2 x[L];
+#pragma unroll
+            for (int k = 0; k < L / 2; ++k) {
+                x[k] = g0[L / 4 + k];
+                x[L / 2 + k] = g1[L / 4 + k];
+            }
+            fft_reg<L, -1>(x);
+            const float2 phs = cscale(ph, sd.rx_s0 / (float)L);
+#pragma unroll
+            for (int b = 0; b < L; ++b) g0[b] = cmul(x[b], phs);
+        }
+#pragma unroll
+        for (int b = 0; b < L; ++b) {
+            if (P.grid_full) {
+                orow[sd.full_off + b] = g0[b];
+            } else {
+                const int a = __ldg(&P.inv[sd.full_off + b]);
+                if (a >= 0) orow[sd.act_off + a] = g0[b];
+            }
+        }
+    }
+}
+
+template <int N, int L>
+FCW_DI void rx_short_warp(const KParams& P, const SymDev& sy, const float2* spec0, const float2* spec1,
+                          float2* __restrict__ orow, float2* scr, int gstart, int gcount) {
+    constexpr int PPT = L / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    float2* const b1[1] = {scr};
+    for (int i = warp; i < gcount; i += kWarps) {
+        const int m = P.grp_sub ? __ldg(&P.grp_sub[gstart + i]) : gstart + i;
+        const SubDev sd = P.sub[m];
+        float2 g0[1][PPT], g1[1][PPT];
+        int inv[PPT];
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) {
+            const int b = lane + 32 * k;
+            const int4 e = bin_entry(P, sd, b);
+            inv[k] = e.x;
+            const int q = (sd.c - L / 2 + (b ^ (L / 2))) & (N - 1);
+            g0[0][k] = cscale(spec0[q], __int_as_float(e.z));
+            g1[0][k] = cscale(spec1[q], __int_as_float(e.w));
+        }
+        const float2 ph = __ldg(&P.tw[theta_exp<N>(sd.cmodN, sy.smodN)]);
+        if (P.fused) {
+            const bool odd = lane & 1;
+#pragma unroll
+            for (int k = 0; k < PPT; ++k) {
+                if (odd) g1[0][k] = make_float2(-g1[0][k].x, -g1[0][k].y);  // t
+                g0[0][k] = mul_jpow_rt(csub(g0[0][k], g1[0][k]), lane);
+            }
+            team_fft<L, 32, PPT, +1, 1, false>(g0, b1, P.tw, N / L, lane, true);
+#pragma unroll
+            for (int k = PPT / 2; k < PPT; ++k) g0[0][k] = zero2();
+            team_fft<L, 32, PPT, -1, 1, false>(g0, b1, P.tw, N / L, lane, true);
+            const float a = sd.rx_s0 / (float)L, s = sd.rx_s0;
+#pragma unroll
+            for (int k = 0; k < PPT; ++k) {
+                const float2 tj = mul_jpow_rt(g1[0][k], lane);
+                g0[0][k] = cmul(make_float2(fmaf(g0[0][k].x, a, tj.x * s), fmaf(g0[0][k].y, a, tj.y * s)), ph);
+            }
+        } else {
+            team_fft<L, 32, PPT, +1, 1, false>(g0, b1, P.tw, N / L, lane, true);
+            team_fft<L, 32, PPT, +1, 1, false>(g1, b1, P.tw, N / L, lane, true);
+            float2 x[1][PPT];
+            if constexpr (L >= 128) {
+                // central halves: element L/4 + i of block r -> register rename
+#pragma unroll
+                for (int k = 0; k < PPT; ++k)
+                    x[0][k] = (k < PPT / 2) ? g0[0][k + PPT / 4] : g1[0][k - PPT / 2 + PPT / 4];
+            } else {
+                float2* s1 = scr + P.scratch_stride / 2;
+                __syncwarp();
+#pragma unroll
+                for (int k = 0; k < PPT; ++k) {
+                    scr[lane + 32 * k] = g0[0][k];
+                    s1[lane + 32 * k] = g1[0][k];
+                }
+                __syncwarp();
+#pragma unroll
+                for (int k = 0; k < PPT; ++k) {
+                    const int e = lane + 32 * k;
+                    x[0][k] = (k < PPT / 2) ? scr[L / 4 + e] : s1[L / 4 + e - L / 2];
+                }
+            }
+            team_fft<L, 32, PPT, -1, 1, false>(x, b1, P.tw, N / L, lane, true);
+            const float2 phs = cscale(ph, sd.rx_s0 / (float)L);
+#pragma unroll
+            for (int k = 0; k < PPT; ++k) g0[0][k] = cmul(x[0][k], phs);
+        }
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) {
+            const int b = lane + 32 * k;
+            if (P.grid_full)
+                orow[sd.full_off + b] = g0[0][k];
+            else if (inv[k] >= 0)
+                orow[sd.act_off + inv[k]] = g0[0][k];
+        }
+        __syncwarp();
+    }
+}
+
+template <int N, int L>
+FCW_DI void rx_short_one(const KParams& P, const SymDev& sy, const float2* spec0, const float2* spec1,
+                         float2* orow, float2* scr, int gs, int gc) {
+    if constexpr (L <= N) {
+        if constexpr (L <= 32)
+            rx_short_thread<N, L>(P, sy, spec0, spec1, orow, gs, gc);
+        else
+            rx_short_warp<N, L>(P, sy, spec0, spec1, orow, scr, gs, gc);
+    }
+}
+
+template <int N, int LU>
+FCW_DI void rx_short_all(const KParams& P, const SymDev& sy, const float2* spec0, const float2* spec1,
+                         float2* orow, float2* scr) {
+    if constexpr (LU > 0) {
+        rx_short_one<N, LU>(P, sy, spec0, spec1, orow, scr, 0, P.M);
+    } else {
+        for (int g = 0; g < P.n_groups; ++g) {
+            const int gs = P.grp_start[g], gc = P.grp_count[g];
+            switch (P.grp_L[g]) {
+                case 4: rx_short_one<N, 4>(P, sy, spec0, spec1, orow, scr, gs, gc); break;
+                case 8: rx_short_one<N, 8>(P, sy, spec0, spec1, orow, scr, gs, gc); break;
+                case 16: rx_short_one<N, 16>(P, sy, spec0, spec1, orow, scr, gs, gc); break;
+                case 32: rx_short_one<N, 32>(P, sy, spec0, spec1, orow, scr, gs, gc); break;
+                case 64: rx_short_one<N, 64>(P, sy, spec0, spec1, orow, scr, gs, gc); break;
+                case 128: rx_short_one<N, 128>(P, sy, spec0, spec1, orow, scr, gs, gc); break;
+                case 256: rx_short_one<N, 256>(P, sy, spec0, spec1, orow, scr, gs, gc); break;
+                case 512: rx_short_one<N, 512>(P, sy, spec0, spec1, orow, scr, gs, gc); break;
+                case 1024: rx_short_one<N, 1024>(P, sy, spec0, spec1, orow, scr, gs, gc); break;
+                default: break;
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------ kernels
+
+template <int LU>
+constexpr int min_blocks() {
+    return (LU >= 64 || (LU > 0 && LU <= 16)) ? 2 : 1;
+}
+
+template <int N, int LU>
+__global__ void __launch_bounds__(kThreads, min_blocks<LU>()) tx_kernel(const KParams P) {
+    extern __shared__ float4 smem_raw[];
+    float2* sm = reinterpret_cast<float2*>(smem_raw);
+    float2* spec0 = sm;
+    float2* spec1 = sm + P.spec_stride;
+    float2* carry = spec1 + P.spec_stride;
+    float2* scr = carry + N / 2 + (threadIdx.x >> 5) * P.scratch_stride;
+    constexpr int T = N / kPPT;
+    const int tid = threadIdx.x;
+    const bool act = tid < T;
+    const int unit = blockIdx.x / P.nchunks;
+    const int n0 = (blockIdx.x % P.nchunks) * P.chunk;
+    const int n1 = min(P.B, n0 + P.chunk);
+    const float2* in_u = P.in + (long long)unit * P.in_stride;
+    float2* out_u = P.out + (long long)unit * P.out_stride;
+
+    for (int n = n0 > 0 ? n0 - 1 : 0; n < n1; ++n) {
+        const SymDev sy = P.sym[n];
+        __syncthreads();  // previous symbol's transform no longer reads spec
+        tx_short_all<N, LU>(P, sy, in_u + (long long)n * P.row_len, spec0, spec1, scr);
+        __syncthreads();
+        // secondary contributions of shared transition bins, in rank order
+        for (int l = 0; l < P.n_lvl; ++l) {
+            for (int k = P.lvl_start[l] + tid; k < P.lvl_start[l + 1]; k += kThreads) {
+                const int q = __ldg(&P.fix_tgt[k]);
+                spec0[q] = cadd(spec0[q], spec0[N + k]);
+                spec1[q] = cadd(spec1[q], spec1[N + k]);
+            }
+            __syncthreads();
+        }
+        for (int k = tid; k < P.n_zero; k += kThreads) {
+            const int q = __ldg(&P.zero_list[k]);
+            spec0[q] = zero2();
+            spec1[q] = zero2();
+        }
+        __syncthreads();
+
+        float2 cr[8];
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+            const int u = tid + T * m;
+            cr[m] = (act && u < sy.carry_len) ? carry[u] : zero2();
+        }
+        float2 v[2][kPPT];
+        if (act) {
+#pragma unroll
+            for (int m = 0; m < kPPT; ++m) {
+                v[0][m] = spec0[tid + T * m];
+                v[1][m] = spec1[tid + T * m];
+            }
+        }
+        {
+            float2* const bufs[2] = {spec0, spec1};
+            team_fft<N, T, kPPT, +1, 2, true>(v, bufs, P.tw, 1, tid, act);
+        }
+        if constexpr (T == 1) __syncthreads();
+        // symbol-wise overlap-add: block 0 at 0, block 1 at N/2, carry from n-1
+        if (act) {
+            const bool emit = n >= n0;
+            float2* dst = out_u + sy.sigma;
+#pragma unroll
+            for (int mm = 0; mm < 24; ++mm) {
+                const int u = tid + T * mm;
+                float2 val = zero2();
+                if (mm < 16) val = v[0][mm];
+                if (mm >= 8) val = cadd(val, v[1][mm - 8]);
+                if (mm < 8) val = cadd(val, cr[mm]);
+                if (u < sy.own_len) {
+                    if (emit) dst[u] = val;
+                } else {
+                    carry[u - sy.own_len] = val;
+                }
+            }
+        }
+    }
+}
+
+template <int N, int LU>
+__global__ void __launch_bounds__(kThreads, min_blocks<LU>()) rx_kernel(const KParams P) {
+    extern __shared__ float4 smem_raw[];
+    float2* sm = reinterpret_cast<float2*>(smem_raw);
+    float2* spec0 = sm;
+    float2* spec1 = sm + P.spec_stride;
+    float2* scr = spec1 + P.spec_stride + (threadIdx.x >> 5) * P.scratch_stride;
+    constexpr int T = N / kPPT;
+    const int tid = threadIdx.x;
+    const bool act = tid < T;
+    const int unit = blockIdx.x / P.nchunks;
+    const int n0 = (blockIdx.x % P.nchunks) * P.chunk;
+    const int n1 = min(P.B, n0 + P.chunk);
+    const float2* in_u = P.in + (long long)unit * P.in_stride;
+    float2* out_u = P.out + (long long)unit * P.out_stride;
+
+    for (int n = n0; n < n1; ++n) {
+        const SymDev sy = P.sym[n];
+        float2 v[2][kPPT];
+        if (act) {
+            // rx_segment (fc_sync.cpp:145-156): y0 = w[start, +N), y1 = w[start + N/2, +N)
+            const float2* src = in_u + P.rx_base + sy.sigma + tid;
+#pragma unroll
+            for (int mm = 0; mm < 24; ++mm) {
+                const float2 val = __ldg(&src[T * mm]);
+                if (mm < 16) v[0][mm] = val;
+                if (mm >= 8) v[1][mm - 8] = val;
+            }
+        }
+        __syncthreads();  // previous symbol's subband stage no longer reads spec
+        {
+            float2* const bufs[2] = {spec0, spec1};
+            team_fft<N, T, kPPT, -1, 2, true>(v, bufs, P.tw, 1, tid, act);
+        }
+        __syncthreads();
+        if (act) {
+#pragma unroll
+            for (int m = 0; m < kPPT; ++m) {
+                spec0[tid + T * m] = v[0][m];
+                spec1[tid + T * m] = v[1][m];
+            }
+        }
+        __syncthreads();
+        rx_short_all<N, LU>(P, sy, spec0, spec1, out_u + (long long)n * P.row_len, scr);
+    }
+}
+
+// Dispatch tables filled by the per-N instantiation units.
+using KernelFn = void (*)(KParams);
+struct KernelPair {
+    KernelFn tx, rx;
+};
+
+}  // namespace fcw

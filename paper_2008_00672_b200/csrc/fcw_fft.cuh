@@ -152,6 +152,37 @@ FCW_DI void team_bar() {
 
 FCW_DI int spad(int e) { return e + (e >> 4); }
 
+// w[k] = W^(k*e0) for k < R from log2(R) table loads (W^e0, W^2e0, W^4e0,
+// W^8e0) and at most two products each, so every power carries at most ~3 ulp
+// of rounding (a plain k-step recurrence would grow linearly in k).
+// tw is the plan table exp(-2 pi i m / N); e0 is already in table units and
+// k*e0 < N for every k < R.
+template <int R, int SIGN>
+FCW_DI void twiddle_powers(float2 (&w)[R], const float2* __restrict__ tw, int e0) {
+    auto ld = [&](int e) {
+        float2 v = __ldg(&tw[e]);
+        if constexpr (SIGN > 0) v.y = -v.y;
+        return v;
+    };
+    w[0] = make_float2(1.f, 0.f);
+    if constexpr (R >= 2) w[1] = ld(e0);
+    if constexpr (R >= 4) {
+        w[2] = ld(2 * e0);
+        w[3] = cmul(w[1], w[2]);
+    }
+    if constexpr (R >= 8) {
+        w[4] = ld(4 * e0);
+        w[5] = cmul(w[1], w[4]);
+        w[6] = cmul(w[2], w[4]);
+        w[7] = cmul(w[3], w[4]);
+    }
+    if constexpr (R >= 16) {
+        w[8] = ld(8 * e0);
+#pragma unroll
+        for (int k = 9; k < 16; ++k) w[k] = cmul(w[k - 8], w[8]);
+    }
+}
+
 // One Stockham pass (and the remaining ones, recursively).
 template <int n, int T, int PPT, int SIGN, int NF, bool CTA, int NS>
 FCW_DI void team_pass(float2 (&v)[NF][PPT], float2* const* buf, const float2* __restrict__ tw,
@@ -173,14 +204,12 @@ FCW_DI void team_pass(float2 (&v)[NF][PPT], float2* const* buf, const float2* __
                 for (int k = 0; k < R; ++k) y[f][k] = v[f][i + k * NB];
             if constexpr (NS > 1) {
                 const int jm = j & (NS - 1);
+                float2 wk[R];
+                twiddle_powers<R, SIGN>(wk, tw, jm * (n / (NS * R)) * ts);
 #pragma unroll
-                for (int k = 1; k < R; ++k) {
-                    const int e = jm * k * (n / (NS * R));
-                    float2 w = __ldg(&tw[e * ts]);
-                    if constexpr (SIGN > 0) w.y = -w.y;
+                for (int k = 1; k < R; ++k)
 #pragma unroll
-                    for (int f = 0; f < NF; ++f) y[f][k] = cmul(y[f][k], w);
-                }
+                    for (int f = 0; f < NF; ++f) y[f][k] = cmul(y[f][k], wk[k]);
             }
 #pragma unroll
             for (int f = 0; f < NF; ++f) fft_reg<R, SIGN>(y[f]);

@@ -62,9 +62,8 @@ struct KParams {
     long long in_stride, out_stride;
     const SubDev* sub;
     const SymDev* sym;
-    const float* win;    // [sum L] shifted-domain window per subband
     const int* inv;      // [sum L] DFT bin -> active index or -1
-    const int* dest;     // [sum L] shifted index p0 -> spectrum slot (q or N + ext) or -1
+    const int4* bin;     // [sum L] per DFT bin b: {inv[b], dest[p0], bits(w[p0]), bits(w[p0]*bp1)}, p0 = b ^ L/2
     const int* grp_sub;  // subband ids grouped by L
     const int* fix_tgt;  // [n_ext] target bin of each secondary contribution
     const int* zero_list;  // [n_zero] bins no subband touches
@@ -95,6 +94,7 @@ struct Plan {
     std::vector<SymDev> h_sym;
     std::vector<float> h_win;
     std::vector<int> h_inv, h_dest, h_grp_sub, h_fix, h_zero;
+    std::vector<int4> h_bin;
     int n_ext = 0, n_lvl = 0;
     std::vector<int> lvl_start;
     int n_groups = 0;
@@ -104,8 +104,8 @@ struct Plan {
     void* d_blob = nullptr;
     SubDev* d_sub = nullptr;
     SymDev* d_sym = nullptr;
-    float* d_win = nullptr;
-    int *d_inv = nullptr, *d_dest = nullptr, *d_grp_sub = nullptr, *d_fix = nullptr, *d_zero = nullptr;
+    int *d_inv = nullptr, *d_grp_sub = nullptr, *d_fix = nullptr, *d_zero = nullptr;
+    int4* d_bin = nullptr;
     float2* d_tw = nullptr;
     // host-buffer pipeline state
     std::mutex host_mu;
@@ -114,7 +114,7 @@ struct Plan {
     size_t stage_bytes[2][2] = {{0, 0}, {0, 0}};
 };
 
-// kernels.cu
+// fcw_launch.cu
 cudaError_t launch_tx(const Plan& plan, KParams& kp, int S, cudaStream_t st);
 cudaError_t launch_rx(const Plan& plan, KParams& kp, int S, cudaStream_t st);
 cudaError_t launch_gen_qam(const Plan& plan, uint64_t seed, long long unit0, int S, int bits,

@@ -1,0 +1,27 @@
+// Instantiation helpers: each fcw_k_*.cu unit instantiates the kernels of a
+// few long-transform sizes so nvcc runs them in parallel.
+#pragma once
+
+#include "fcw_device.cuh"
+
+#define FCW_SPEC(NN, LL) \
+    case LL:             \
+        return KernelPair{tx_kernel<NN, LL>, rx_kernel<NN, LL>};
+
+// Generic (mixed-L) kernel plus uniform-L specialisations for the common sizes.
+#define FCW_KERNELS_FULL(NN)                                                   \
+    KernelPair kernels_n##NN(int LU) {                                         \
+        switch (LU) {                                                          \
+            FCW_SPEC(NN, 16)                                                   \
+            FCW_SPEC(NN, 32)                                                   \
+            FCW_SPEC(NN, 64)                                                   \
+            FCW_SPEC(NN, 128)                                                  \
+            FCW_SPEC(NN, 256)                                                  \
+            FCW_SPEC(NN, 512)                                                  \
+            FCW_SPEC(NN, 1024)                                                 \
+            default: return KernelPair{tx_kernel<NN, 0>, rx_kernel<NN, 0>};    \
+        }                                                                      \
+    }
+
+#define FCW_KERNELS_GENERIC(NN) \
+    KernelPair kernels_n##NN(int) { return KernelPair{tx_kernel<NN, 0>, rx_kernel<NN, 0>}; }

@@ -1,0 +1,161 @@
+// Launch configuration and the K-GEN generator kernel.
+#include "fcw_device.cuh"
+
+namespace fcw {
+
+KernelPair kernels_n16(int);
+KernelPair kernels_n32(int);
+KernelPair kernels_n64(int);
+KernelPair kernels_n128(int);
+KernelPair kernels_n256(int);
+KernelPair kernels_n512(int);
+KernelPair kernels_n1024(int);
+KernelPair kernels_n2048(int);
+KernelPair kernels_n4096(int);
+
+namespace {
+
+KernelPair pick(int N, int LU) {
+    switch (N) {
+        case 16: return kernels_n16(LU);
+        case 32: return kernels_n32(LU);
+        case 64: return kernels_n64(LU);
+        case 128: return kernels_n128(LU);
+        case 256: return kernels_n256(LU);
+        case 512: return kernels_n512(LU);
+        case 1024: return kernels_n1024(LU);
+        case 2048: return kernels_n2048(LU);
+        case 4096: return kernels_n4096(LU);
+        default: return KernelPair{nullptr, nullptr};
+    }
+}
+
+// The uniform short size the specialised kernels were built for, or 0.
+int uniform_L(const Plan& p) {
+    if (p.n_groups != 1 || p.N < 1024) return 0;
+    const int L = p.grp_L[0];
+    return (L >= 16 && L <= 1024) ? L : 0;
+}
+
+int spec_stride(const Plan& p) {
+    const int ext = p.n_ext > p.N / 16 ? p.n_ext : p.N / 16;
+    return (p.N + ext + 2 + 1) & ~1;
+}
+
+// Warp scratch: one padded buffer of the largest warp-path L, two where a path
+// needs both blocks' short outputs at once (direct RX at L = 64, generic).
+int scratch_stride(const Plan& p, int LU, bool rx_direct) {
+    if (p.Lmax < 64) return 0;
+    const int one = (p.Lmax + p.Lmax / 16 + 2 + 1) & ~1;
+    const bool two = rx_direct && (LU == 0 || LU == 64 || p.Lmax == 64);
+    return two ? 2 * one : one;
+}
+
+size_t smem_bytes(const Plan& p, bool tx, bool rx_direct) {
+    const int LU = uniform_L(p);
+    const size_t f2 = 2 * (size_t)spec_stride(p) + (tx ? p.N / 2 : 0) +
+                      (size_t)kWarps * scratch_stride(p, LU, rx_direct);
+    return f2 * sizeof(float2);
+}
+
+cudaError_t launch_one(KernelFn k, size_t smem, int grid, const KParams& kp, cudaStream_t st) {
+    if (!k) return cudaErrorInvalidValue;
+    cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(k),
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    void* args[] = {const_cast<KParams*>(&kp)};
+    return cudaLaunchKernel(reinterpret_cast<const void*>(k), dim3(grid), dim3(kThreads), args, smem, st);
+}
+
+}  // namespace
+
+void fill_common(const Plan& p, KParams& kp) {
+    kp.N = p.N;
+    kp.B = p.B;
+    kp.M = p.M;
+    kp.spec_stride = spec_stride(p);
+    kp.n_ext = p.n_ext;
+    kp.n_zero = (int)p.h_zero.size();
+    kp.n_lvl = p.n_lvl;
+    for (int i = 0; i <= kMaxLevels; ++i) kp.lvl_start[i] = i < (int)p.lvl_start.size() ? p.lvl_start[i] : p.n_ext;
+    kp.n_groups = p.n_groups;
+    for (int g = 0; g < kMaxGroups; ++g) {
+        kp.grp_L[g] = p.grp_L[g];
+        kp.grp_start[g] = p.grp_start[g];
+        kp.grp_count[g] = p.grp_count[g];
+    }
+    kp.Q = p.Q;
+    kp.sub = p.d_sub;
+    kp.sym = p.d_sym;
+    kp.inv = p.d_inv;
+    kp.bin = p.d_bin;
+    // uniform-L plans iterate subbands directly (identity group order)
+    kp.grp_sub = uniform_L(p) ? nullptr : p.d_grp_sub;
+    kp.fix_tgt = p.d_fix;
+    kp.zero_list = p.d_zero;
+    kp.tw = p.d_tw;
+}
+
+size_t tx_smem_bytes(const Plan& p) { return smem_bytes(p, true, false); }
+size_t rx_smem_bytes(const Plan& p) { return smem_bytes(p, false, true); }
+
+cudaError_t launch_tx(const Plan& p, KParams& kp, int S, cudaStream_t st) {
+    const int LU = uniform_L(p);
+    kp.scratch_stride = scratch_stride(p, LU, false);
+    return launch_one(pick(p.N, LU).tx, smem_bytes(p, true, false), S * kp.nchunks, kp, st);
+}
+
+cudaError_t launch_rx(const Plan& p, KParams& kp, int S, cudaStream_t st) {
+    const int LU = uniform_L(p);
+    const bool direct = !kp.fused;
+    kp.scratch_stride = scratch_stride(p, LU, direct);
+    return launch_one(pick(p.N, LU).rx, smem_bytes(p, false, direct), S * kp.nchunks, kp, st);
+}
+
+// K-GEN: one thread per QAM symbol; splitmix64 is counter-based, so draw j of
+// unit u is mix(seed_u + (j+1) * gamma) and every draw is independent
+// (channel.cpp:19-48, scenario.cpp:110-128, ofdm.cpp:55-65).
+__global__ void gen_qam_kernel(uint64_t seed, long long unit0, int S, long long per_unit, int bits,
+                               float2* __restrict__ out) {
+    const long long total = (long long)S * per_unit;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const long long u = idx / per_unit, i = idx - u * per_unit;
+        uint64_t s = seed ^ (0x9e3779b97f4a7c15ULL * (uint64_t)(unit0 + u + 1));  // derive_seed
+        s += 0x9e3779b97f4a7c15ULL;
+        uint64_t z = s;
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+        uint64_t st = z ^ (z >> 31);
+        if (st == 0) st = 0x1234567890abcdefULL;  // GaussianRng ctor (channel.cpp:26)
+        unsigned sym = 0;
+        const uint64_t base = st + (uint64_t)(i * bits) * 0x9e3779b97f4a7c15ULL;
+        for (int b = 0; b < bits; ++b) {
+            uint64_t x = base + (uint64_t)(b + 1) * 0x9e3779b97f4a7c15ULL;
+            x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+            x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+            x ^= x >> 31;
+            sym |= (unsigned)(x & 1u) << b;
+        }
+        const int k = bits / 2, levels = 1 << k;
+        const unsigned mask = (1u << k) - 1u;
+        unsigned gi = sym & mask, gq = (sym >> k) & mask, li = 0, lq = 0;
+        for (; gi; gi >>= 1) li ^= gi;
+        for (; gq; gq >>= 1) lq ^= gq;
+        const double sc = 1.0 / sqrt(2.0 * ((double)levels * levels - 1.0) / 3.0);
+        out[idx] = make_float2((float)(sc * (2.0 * li + 1 - levels)), (float)(sc * (2.0 * lq + 1 - levels)));
+    }
+}
+
+cudaError_t launch_gen_qam(const Plan& p, uint64_t seed, long long unit0, int S, int bits, float2* out,
+                           cudaStream_t st) {
+    const long long per_unit = (long long)p.B * p.row_active;
+    const long long total = per_unit * S;
+    int grid = (int)((total + 255) / 256);
+    if (grid > 148 * 64) grid = 148 * 64;
+    if (grid < 1) grid = 1;
+    gen_qam_kernel<<<grid, 256, 0, st>>>(seed, unit0, S, per_unit, bits, out);
+    return cudaGetLastError();
+}
+
+}  // namespace fcw

@@ -97,3 +97,100 @@ def test_rx_parity(case, fused):
     for u in range(S):
         assert rel_rms(out_p[u].cpu().numpy(), wants_p[u]) <= TOL
         assert rel_rms(out_f[u].cpu().numpy(), wants_f[u]) <= TOL
+
+
+# ---------------------------------------------------------------- generic path
+def _golden():
+    d = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    return sorted(os.path.join(d, f) for f in os.listdir(d) if f.endswith(".npz"))
+
+
+@pytest.mark.parametrize("path", _golden(), ids=lambda p: os.path.basename(p)[:-4])
+def test_gpu_matches_reference_golden(path):
+    """The committed outputs of the UNMODIFIED reference (tests/golden) — full
+    DFT-bin grids in, reference waveform / RX columns out."""
+    z = np.load(path)
+    N, cp = int(z["N"]), z["cp"].tolist()
+    Ls, cs = z["Ls"].tolist(), z["cs"].tolist()
+    wins = np.split(z["windows"], np.cumsum(Ls)[:-1])
+    B = len(cp)
+    subs = [api.SubbandConfig(L=L, c=c, window=w) for L, c, w in zip(Ls, cs, wins)]
+    plan = api.Plan(N, cp, subs)
+    grids = np.split(z["grids"], np.cumsum([B * L for L in Ls])[:-1])
+    rows = np.concatenate([g.reshape(B, L) for g, L in zip(grids, Ls)], axis=1)
+    wave = plan.tx_host(rows.reshape(-1), 1, full=True)[0]
+    assert plan.Q == len(z["wave"]) and plan.useful0 == int(z["useful0"])
+    assert rel_rms(wave, z["wave"]) <= TOL
+    for fused in (0, 1):
+        got = plan.rx_host(z["wave"].astype(np.complex64), plan.Q, plan.useful0, 1, fused=bool(fused), full=True)[0]
+        off = 0
+        for m, L in enumerate(Ls):
+            assert rel_rms(got[:, off:off + L], z[f"rx_{m}_{fused}"]) <= TOL, (m, fused)
+            off += L
+
+
+def _random_case(rng, N, Ls, cps):
+    subs, maps = [], []
+    for L in Ls:
+        c = int(rng.integers(0, N))
+        subs.append(api.SubbandConfig(L=L, c=c, window=rng.uniform(0, 1, L)))
+        maps.append(sorted(rng.choice(L, size=max(1, L // 2), replace=False).tolist()))
+    return subs, maps
+
+
+@pytest.mark.parametrize("N,Ls,cps", [
+    (32, [8], [8, 4, 4, 4]),
+    (16, [16], [2, 1, 1]),
+    (64, [16, 8, 4], [8, 4, 4, 8, 4]),
+    (256, [32, 64, 16, 64], [16, 12, 12, 12, 16, 12]),
+    (1024, [16, 64, 256], [80, 72, 72, 72]),     # mixed L at a specialised N -> generic kernel
+    (2048, [1024, 512], [144] * 6),
+    (4096, [32] * 7, [352, 288, 288, 288]),
+    (4096, [1024, 64], [352, 288, 288]),
+])
+def test_random_geometries(N, Ls, cps):
+    rng = np.random.default_rng(N + len(Ls))
+    subs, maps = _random_case(rng, N, Ls, cps)
+    B = len(cps)
+    plan = api.Plan(N, cps, subs, maps)
+    S = 3
+    grid = (rng.standard_normal((S, B, plan.row_active)) + 1j * rng.standard_normal((S, B, plan.row_active)))
+    grid = grid.astype(np.complex64)
+    wave = plan.tx_host(grid, S)
+    w = type("W", (), {})()
+    w.subbands, w.active_maps, w.B, w.N, w.cp = subs, maps, B, N, cps
+    for u in range(S):
+        want, u0 = oracle_tx(w, grid[u].astype(np.complex128))
+        assert rel_rms(wave[u], want) <= TOL, u
+    for fused in (False, True):
+        out = plan.rx_host(wave, plan.Q, plan.useful0, S, fused=fused)
+        for u in range(S):
+            want_p, _ = oracle_rx(w, wave[u].astype(np.complex128), plan.useful0, fused)
+            assert rel_rms(out[u], want_p) <= TOL, (u, fused)
+
+
+@pytest.mark.parametrize("chunk", ["1", "3", "7", "280"])
+def test_chunk_boundaries_full_frame(chunk, monkeypatch):
+    """Full 280-symbol C5 frame: every CTA-run boundary recomputes the carry of
+    the symbol before it; results must not depend on the run length."""
+    monkeypatch.setenv("FCW_CHUNK", chunk)
+    w = configs.config5()
+    plan = w.plan()
+    grid = torch.empty((1, w.B, plan.row_active), dtype=torch.complex64, device="cuda")
+    plan.gen_qam(SEED, 5, 1, w.bits_per_symbol, grid)
+    wave = torch.empty((1, plan.Q), dtype=torch.complex64, device="cuda")
+    plan.tx(grid, wave, 1)
+    out = torch.empty_like(grid)
+    plan.rx(wave, plan.Q, plan.useful0, out, 1, fused=True)
+    torch.cuda.synchronize()
+    key = ("c5full",)
+    if key not in _FULL:
+        g = grid[0].cpu().numpy().astype(np.complex128)
+        ww, u0 = oracle_tx(w, g)
+        _FULL[key] = (ww, oracle_rx(w, wave[0].cpu().numpy().astype(np.complex128), u0, True)[0])
+    want_w, want_r = _FULL[key]
+    assert rel_rms(wave[0].cpu().numpy(), want_w) <= TOL
+    assert rel_rms(out[0].cpu().numpy(), want_r) <= TOL
+
+
+_FULL: dict = {}
