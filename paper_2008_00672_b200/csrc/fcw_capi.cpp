@@ -314,6 +314,10 @@ int fcw_plan_create(fcw_plan** out, int N, double overlap, const int* cp_high, i
     std::stable_sort(secondary.begin(), secondary.end(),
                      [](const Contrib& a, const Contrib& b) { return a.rank < b.rank; });
     int max_rank = secondary.empty() ? 0 : secondary.back().rank;
+    if (N + (long long)secondary.size() >= 32768) {
+        delete p;
+        return fail(FCW_ENOTSUP, "too many shared transition bins for the 16-bit spectrum slot index");
+    }
     if (max_rank > fcw::kMaxLevels) {
         delete p;
         return fail(FCW_ENOTSUP, "more than 9 subbands share one N-grid bin");
@@ -362,12 +366,10 @@ int fcw_plan_create(fcw_plan** out, int N, double overlap, const int* cp_high, i
         for (int b = 0; b < d.L; ++b) {
             const int p0 = b ^ (d.L / 2);
             const float w = p->h_win[d.full_off + p0];
-            const float w1 = w * d.bp1;
-            int4 e;
-            e.x = p->h_inv[d.full_off + b];
-            e.y = p->h_dest[d.full_off + p0];
-            std::memcpy(&e.z, &w, 4);
-            std::memcpy(&e.w, &w1, 4);
+            const int inv = p->h_inv[d.full_off + b], dest = p->h_dest[d.full_off + p0];
+            int2 e;
+            e.x = (inv & 0xffff) | (int)((unsigned)dest << 16);
+            std::memcpy(&e.y, &w, 4);
             p->h_bin[d.full_off + b] = e;
         }
     }
@@ -384,7 +386,7 @@ int fcw_plan_create(fcw_plan** out, int N, double overlap, const int* cp_high, i
     const size_t o_sym = off;
     off = align(off + sizeof(fcw::SymDev) * B);
     const size_t o_bin = off;
-    off = align(off + sizeof(int4) * p->h_bin.size());
+    off = align(off + sizeof(int2) * p->h_bin.size());
     const size_t o_inv = off;
     off = align(off + sizeof(int) * p->h_inv.size());
     const size_t o_grp = off;
@@ -398,7 +400,7 @@ int fcw_plan_create(fcw_plan** out, int N, double overlap, const int* cp_high, i
     std::vector<unsigned char> host(off, 0);
     std::memcpy(&host[o_sub], p->h_sub.data(), sizeof(fcw::SubDev) * M);
     std::memcpy(&host[o_sym], p->h_sym.data(), sizeof(fcw::SymDev) * B);
-    std::memcpy(&host[o_bin], p->h_bin.data(), sizeof(int4) * p->h_bin.size());
+    std::memcpy(&host[o_bin], p->h_bin.data(), sizeof(int2) * p->h_bin.size());
     std::memcpy(&host[o_inv], p->h_inv.data(), sizeof(int) * p->h_inv.size());
     std::memcpy(&host[o_grp], p->h_grp_sub.data(), sizeof(int) * p->h_grp_sub.size());
     if (!p->h_fix.empty()) std::memcpy(&host[o_fix], p->h_fix.data(), sizeof(int) * p->h_fix.size());
@@ -418,7 +420,7 @@ int fcw_plan_create(fcw_plan** out, int N, double overlap, const int* cp_high, i
     auto* base = static_cast<unsigned char*>(p->d_blob);
     p->d_sub = reinterpret_cast<fcw::SubDev*>(base + o_sub);
     p->d_sym = reinterpret_cast<fcw::SymDev*>(base + o_sym);
-    p->d_bin = reinterpret_cast<int4*>(base + o_bin);
+    p->d_bin = reinterpret_cast<int2*>(base + o_bin);
     p->d_inv = reinterpret_cast<int*>(base + o_inv);
     p->d_grp_sub = reinterpret_cast<int*>(base + o_grp);
     p->d_fix = reinterpret_cast<int*>(base + o_fix);

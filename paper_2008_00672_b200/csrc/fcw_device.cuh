@@ -31,10 +31,31 @@ namespace fcw {
 
 constexpr int kPPT = 16;  // long-transform points per thread and block
 
-// Bin-table entry (plan, per subband and DFT bin b):
-//   x = inv[b] (active index of bin b or -1), y = dest[p0(b)] (spectrum slot or -1),
-//   z = bits(w[p0(b)]), w = bits(w[p0(b)] * bp1), with p0(b) = b ^ L/2.
-FCW_DI int4 bin_entry(const KParams& P, const SubDev& sd, int b) { return __ldg(&P.bin[sd.full_off + b]); }
+// Bin-table entry (plan, per subband and DFT bin b), 8 bytes:
+//   x = (inv[b] & 0xffff) | dest[p0(b)] << 16  (active index / spectrum slot, -1 = none),
+//   y = bits(w[p0(b)]), with p0(b) = b ^ L/2.
+struct Bin {
+    int inv, dest;
+    float w;
+};
+FCW_DI Bin bin_entry(const KParams& P, const SubDev& sd, int b) {
+    const int2 e = __ldg(&P.bin[sd.full_off + b]);
+    return Bin{(int)(short)(e.x & 0xffff), e.x >> 16, __int_as_float(e.y)};
+}
+
+// Bulk L2 prefetch of [p, p + bytes) by one thread (cp.async.bulk, sm_90+):
+// the next symbol's input is on its way from HBM while this one computes.
+FCW_DI void prefetch_l2(const void* p, long long bytes) {
+    // the instruction takes a .global-space address, not a generic one
+    const unsigned long long g = static_cast<unsigned long long>(__cvta_generic_to_global(p));
+    unsigned long long a = g & ~15ull;
+    const unsigned long long e = (g + (unsigned long long)bytes + 15ull) & ~15ull;
+    while (a < e) {
+        const unsigned chunk = (e - a) > (1ull << 20) ? (1u << 20) : (unsigned)(e - a);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(chunk) : "memory");
+        a += chunk;
+    }
+}
 
 FCW_DI float2 tw_conj(const float2* __restrict__ tw, int e) {
     const float2 w = __ldg(&tw[e]);
@@ -66,7 +87,7 @@ FCW_DI void tx_short_thread(const KParams& P, const SymDev& sy, const float2* __
         float2 x[L];
         const float2 ph = cscale(tw_conj(P.tw, theta_exp<N>(sd.cmodN, sy.smodN)), sd.tx_scale);
 #pragma unroll
-        for (int b = 0; b < L; ++b) x[b] = cmul(grid_val(P, sd, row, b, __ldg(&P.inv[sd.full_off + b])), ph);
+        for (int b = 0; b < L; ++b) x[b] = cmul(grid_val(P, sd, row, b, bin_entry(P, sd, b).inv), ph);
         fft_reg<L, +1>(x);  // ofdm_modulate (scale folded into ph)
         const int lcp = sy.cp >> sd.logI;  // cp_truncate (fc_sync.cpp:26-32)
         float2 u0[L], u1[L];
@@ -82,10 +103,10 @@ FCW_DI void tx_short_thread(const KParams& P, const SymDev& sy, const float2* __
         fft_reg<L, -1>(u1);
 #pragma unroll
         for (int b = 0; b < L; ++b) {
-            const int4 e = bin_entry(P, sd, b);
-            if (e.y >= 0) {
-                spec0[e.y] = cscale(u0[b], __int_as_float(e.z));
-                spec1[e.y] = cscale(u1[b], __int_as_float(e.w));
+            const Bin e = bin_entry(P, sd, b);
+            if (e.dest >= 0) {
+                spec0[e.dest] = cscale(u0[b], e.w);
+                spec1[e.dest] = cscale(u1[b], e.w * sd.bp1);
             }
         }
     }
@@ -95,22 +116,23 @@ FCW_DI void tx_short_thread(const KParams& P, const SymDev& sy, const float2* __
 // lane + 32k.  One padded scratch buffer per warp.
 template <int N, int L>
 FCW_DI void tx_short_warp(const KParams& P, const SymDev& sy, const float2* __restrict__ row,
-                          float2* spec0, float2* spec1, float2* scr, int gstart, int gcount) {
+                          float2* spec0, float2* spec1, float2* scr, const float2* stw, int gstart, int gcount) {
     constexpr int PPT = L / 32;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int sts = P.stab_len / L;
     float2* const b1[1] = {scr};
     for (int i = warp; i < gcount; i += kWarps) {
         const int m = P.grp_sub ? __ldg(&P.grp_sub[gstart + i]) : gstart + i;
         const SubDev sd = P.sub[m];
         const float2 ph = cscale(tw_conj(P.tw, theta_exp<N>(sd.cmodN, sy.smodN)), sd.tx_scale);
-        int4 ent[PPT];
+        Bin ent[PPT];
         float2 v[1][PPT];
 #pragma unroll
         for (int k = 0; k < PPT; ++k) {
             ent[k] = bin_entry(P, sd, lane + 32 * k);
-            v[0][k] = cmul(grid_val(P, sd, row, lane + 32 * k, ent[k].x), ph);
+            v[0][k] = cmul(grid_val(P, sd, row, lane + 32 * k, ent[k].inv), ph);
         }
-        team_fft<L, 32, PPT, +1, 1, false>(v, b1, P.tw, N / L, lane, true);
+        team_fft<L, 32, PPT, +1, 1, false>(v, b1, stw, sts, lane, true);
         const int lcp = sy.cp >> sd.logI;
         float2 u0[1][PPT], u1[1][PPT];
         if constexpr (L >= 128) {
@@ -137,46 +159,46 @@ FCW_DI void tx_short_warp(const KParams& P, const SymDev& sy, const float2* __re
                 u1[0][k] = in1 ? scr[(e + L / 4) & (L - 1)] : zero2();
             }
         }
-        team_fft<L, 32, PPT, -1, 1, false>(u0, b1, P.tw, N / L, lane, true);
+        team_fft<L, 32, PPT, -1, 1, false>(u0, b1, stw, sts, lane, true);
 #pragma unroll
         for (int k = 0; k < PPT; ++k)
-            if (ent[k].y >= 0) spec0[ent[k].y] = cscale(u0[0][k], __int_as_float(ent[k].z));
-        team_fft<L, 32, PPT, -1, 1, false>(u1, b1, P.tw, N / L, lane, true);
+            if (ent[k].dest >= 0) spec0[ent[k].dest] = cscale(u0[0][k], ent[k].w);
+        team_fft<L, 32, PPT, -1, 1, false>(u1, b1, stw, sts, lane, true);
 #pragma unroll
         for (int k = 0; k < PPT; ++k)
-            if (ent[k].y >= 0) spec1[ent[k].y] = cscale(u1[0][k], __int_as_float(ent[k].w));
+            if (ent[k].dest >= 0) spec1[ent[k].dest] = cscale(u1[0][k], ent[k].w * sd.bp1);
     }
 }
 
 template <int N, int L>
 FCW_DI void tx_short_one(const KParams& P, const SymDev& sy, const float2* __restrict__ row, float2* spec0,
-                         float2* spec1, float2* scr, int gs, int gc) {
+                         float2* spec1, float2* scr, const float2* stw, int gs, int gc) {
     if constexpr (L <= N) {
         if constexpr (L <= 32)
             tx_short_thread<N, L>(P, sy, row, spec0, spec1, gs, gc);
         else
-            tx_short_warp<N, L>(P, sy, row, spec0, spec1, scr, gs, gc);
+            tx_short_warp<N, L>(P, sy, row, spec0, spec1, scr, stw, gs, gc);
     }
 }
 
 template <int N, int LU>
 FCW_DI void tx_short_all(const KParams& P, const SymDev& sy, const float2* __restrict__ row, float2* spec0,
-                         float2* spec1, float2* scr) {
+                         float2* spec1, float2* scr, const float2* stw) {
     if constexpr (LU > 0) {
-        tx_short_one<N, LU>(P, sy, row, spec0, spec1, scr, 0, P.M);
+        tx_short_one<N, LU>(P, sy, row, spec0, spec1, scr, stw, 0, P.M);
     } else {
         for (int g = 0; g < P.n_groups; ++g) {
             const int gs = P.grp_start[g], gc = P.grp_count[g];
             switch (P.grp_L[g]) {
-                case 4: tx_short_one<N, 4>(P, sy, row, spec0, spec1, scr, gs, gc); break;
-                case 8: tx_short_one<N, 8>(P, sy, row, spec0, spec1, scr, gs, gc); break;
-                case 16: tx_short_one<N, 16>(P, sy, row, spec0, spec1, scr, gs, gc); break;
-                case 32: tx_short_one<N, 32>(P, sy, row, spec0, spec1, scr, gs, gc); break;
-                case 64: tx_short_one<N, 64>(P, sy, row, spec0, spec1, scr, gs, gc); break;
-                case 128: tx_short_one<N, 128>(P, sy, row, spec0, spec1, scr, gs, gc); break;
-                case 256: tx_short_one<N, 256>(P, sy, row, spec0, spec1, scr, gs, gc); break;
-                case 512: tx_short_one<N, 512>(P, sy, row, spec0, spec1, scr, gs, gc); break;
-                case 1024: tx_short_one<N, 1024>(P, sy, row, spec0, spec1, scr, gs, gc); break;
+                case 4: tx_short_one<N, 4>(P, sy, row, spec0, spec1, scr, stw, gs, gc); break;
+                case 8: tx_short_one<N, 8>(P, sy, row, spec0, spec1, scr, stw, gs, gc); break;
+                case 16: tx_short_one<N, 16>(P, sy, row, spec0, spec1, scr, stw, gs, gc); break;
+                case 32: tx_short_one<N, 32>(P, sy, row, spec0, spec1, scr, stw, gs, gc); break;
+                case 64: tx_short_one<N, 64>(P, sy, row, spec0, spec1, scr, stw, gs, gc); break;
+                case 128: tx_short_one<N, 128>(P, sy, row, spec0, spec1, scr, stw, gs, gc); break;
+                case 256: tx_short_one<N, 256>(P, sy, row, spec0, spec1, scr, stw, gs, gc); break;
+                case 512: tx_short_one<N, 512>(P, sy, row, spec0, spec1, scr, stw, gs, gc); break;
+                case 1024: tx_short_one<N, 1024>(P, sy, row, spec0, spec1, scr, stw, gs, gc); break;
                 default: break;
             }
         }
@@ -196,10 +218,10 @@ FCW_DI void rx_short_thread(const KParams& P, const SymDev& sy, const float2* sp
         float2 g0[L], g1[L];
 #pragma unroll
         for (int b = 0; b < L; ++b) {
-            const int4 e = bin_entry(P, sd, b);
+            const float w = bin_entry(P, sd, b).w;
             const int q = (sd.c - L / 2 + (b ^ (L / 2))) & (N - 1);
-            g0[b] = cscale(spec0[q], __int_as_float(e.z));
-            g1[b] = cscale(spec1[q], __int_as_float(e.w));
+            g0[b] = cscale(spec0[q], w);
+            g1[b] = cscale(spec1[q], w * sd.bp1);
         }
         const float2 ph = __ldg(&P.tw[theta_exp<N>(sd.cmodN, sy.smodN)]);  // conj(theta_n)
         if (P.fused) {
@@ -252,7 +274,7 @@ FCW_DI void rx_short_thread(const KParams& P, const SymDev& sy, const float2* sp
             if (P.grid_full) {
                 orow[sd.full_off + b] = g0[b];
             } else {
-                const int a = __ldg(&P.inv[sd.full_off + b]);
+                const int a = bin_entry(P, sd, b).inv;
                 if (a >= 0) orow[sd.act_off + a] = g0[b];
             }
         }
@@ -261,9 +283,10 @@ FCW_DI void rx_short_thread(const KParams& P, const SymDev& sy, const float2* sp
 
 template <int N, int L>
 FCW_DI void rx_short_warp(const KParams& P, const SymDev& sy, const float2* spec0, const float2* spec1,
-                          float2* __restrict__ orow, float2* scr, int gstart, int gcount) {
+                          float2* __restrict__ orow, float2* scr, const float2* stw, int gstart, int gcount) {
     constexpr int PPT = L / 32;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int sts = P.stab_len / L;
     float2* const b1[1] = {scr};
     for (int i = warp; i < gcount; i += kWarps) {
         const int m = P.grp_sub ? __ldg(&P.grp_sub[gstart + i]) : gstart + i;
@@ -273,11 +296,11 @@ FCW_DI void rx_short_warp(const KParams& P, const SymDev& sy, const float2* spec
 #pragma unroll
         for (int k = 0; k < PPT; ++k) {
             const int b = lane + 32 * k;
-            const int4 e = bin_entry(P, sd, b);
-            inv[k] = e.x;
+            const Bin e = bin_entry(P, sd, b);
+            inv[k] = e.inv;
             const int q = (sd.c - L / 2 + (b ^ (L / 2))) & (N - 1);
-            g0[0][k] = cscale(spec0[q], __int_as_float(e.z));
-            g1[0][k] = cscale(spec1[q], __int_as_float(e.w));
+            g0[0][k] = cscale(spec0[q], e.w);
+            g1[0][k] = cscale(spec1[q], e.w * sd.bp1);
         }
         const float2 ph = __ldg(&P.tw[theta_exp<N>(sd.cmodN, sy.smodN)]);
         if (P.fused) {
@@ -287,10 +310,10 @@ FCW_DI void rx_short_warp(const KParams& P, const SymDev& sy, const float2* spec
                 if (odd) g1[0][k] = make_float2(-g1[0][k].x, -g1[0][k].y);  // t
                 g0[0][k] = mul_jpow_rt(csub(g0[0][k], g1[0][k]), lane);
             }
-            team_fft<L, 32, PPT, +1, 1, false>(g0, b1, P.tw, N / L, lane, true);
+            team_fft<L, 32, PPT, +1, 1, false>(g0, b1, stw, sts, lane, true);
 #pragma unroll
             for (int k = PPT / 2; k < PPT; ++k) g0[0][k] = zero2();
-            team_fft<L, 32, PPT, -1, 1, false>(g0, b1, P.tw, N / L, lane, true);
+            team_fft<L, 32, PPT, -1, 1, false>(g0, b1, stw, sts, lane, true);
             const float a = sd.rx_s0 / (float)L, s = sd.rx_s0;
 #pragma unroll
             for (int k = 0; k < PPT; ++k) {
@@ -298,8 +321,8 @@ FCW_DI void rx_short_warp(const KParams& P, const SymDev& sy, const float2* spec
                 g0[0][k] = cmul(make_float2(fmaf(g0[0][k].x, a, tj.x * s), fmaf(g0[0][k].y, a, tj.y * s)), ph);
             }
         } else {
-            team_fft<L, 32, PPT, +1, 1, false>(g0, b1, P.tw, N / L, lane, true);
-            team_fft<L, 32, PPT, +1, 1, false>(g1, b1, P.tw, N / L, lane, true);
+            team_fft<L, 32, PPT, +1, 1, false>(g0, b1, stw, sts, lane, true);
+            team_fft<L, 32, PPT, +1, 1, false>(g1, b1, stw, sts, lane, true);
             float2 x[1][PPT];
             if constexpr (L >= 128) {
                 // central halves: element L/4 + i of block r -> register rename
@@ -321,7 +344,7 @@ FCW_DI void rx_short_warp(const KParams& P, const SymDev& sy, const float2* spec
                     x[0][k] = (k < PPT / 2) ? scr[L / 4 + e] : s1[L / 4 + e - L / 2];
                 }
             }
-            team_fft<L, 32, PPT, -1, 1, false>(x, b1, P.tw, N / L, lane, true);
+            team_fft<L, 32, PPT, -1, 1, false>(x, b1, stw, sts, lane, true);
             const float2 phs = cscale(ph, sd.rx_s0 / (float)L);
 #pragma unroll
             for (int k = 0; k < PPT; ++k) g0[0][k] = cmul(x[0][k], phs);
@@ -340,33 +363,33 @@ FCW_DI void rx_short_warp(const KParams& P, const SymDev& sy, const float2* spec
 
 template <int N, int L>
 FCW_DI void rx_short_one(const KParams& P, const SymDev& sy, const float2* spec0, const float2* spec1,
-                         float2* orow, float2* scr, int gs, int gc) {
+                         float2* orow, float2* scr, const float2* stw, int gs, int gc) {
     if constexpr (L <= N) {
         if constexpr (L <= 32)
             rx_short_thread<N, L>(P, sy, spec0, spec1, orow, gs, gc);
         else
-            rx_short_warp<N, L>(P, sy, spec0, spec1, orow, scr, gs, gc);
+            rx_short_warp<N, L>(P, sy, spec0, spec1, orow, scr, stw, gs, gc);
     }
 }
 
 template <int N, int LU>
 FCW_DI void rx_short_all(const KParams& P, const SymDev& sy, const float2* spec0, const float2* spec1,
-                         float2* orow, float2* scr) {
+                         float2* orow, float2* scr, const float2* stw) {
     if constexpr (LU > 0) {
-        rx_short_one<N, LU>(P, sy, spec0, spec1, orow, scr, 0, P.M);
+        rx_short_one<N, LU>(P, sy, spec0, spec1, orow, scr, stw, 0, P.M);
     } else {
         for (int g = 0; g < P.n_groups; ++g) {
             const int gs = P.grp_start[g], gc = P.grp_count[g];
             switch (P.grp_L[g]) {
-                case 4: rx_short_one<N, 4>(P, sy, spec0, spec1, orow, scr, gs, gc); break;
-                case 8: rx_short_one<N, 8>(P, sy, spec0, spec1, orow, scr, gs, gc); break;
-                case 16: rx_short_one<N, 16>(P, sy, spec0, spec1, orow, scr, gs, gc); break;
-                case 32: rx_short_one<N, 32>(P, sy, spec0, spec1, orow, scr, gs, gc); break;
-                case 64: rx_short_one<N, 64>(P, sy, spec0, spec1, orow, scr, gs, gc); break;
-                case 128: rx_short_one<N, 128>(P, sy, spec0, spec1, orow, scr, gs, gc); break;
-                case 256: rx_short_one<N, 256>(P, sy, spec0, spec1, orow, scr, gs, gc); break;
-                case 512: rx_short_one<N, 512>(P, sy, spec0, spec1, orow, scr, gs, gc); break;
-                case 1024: rx_short_one<N, 1024>(P, sy, spec0, spec1, orow, scr, gs, gc); break;
+                case 4: rx_short_one<N, 4>(P, sy, spec0, spec1, orow, scr, stw, gs, gc); break;
+                case 8: rx_short_one<N, 8>(P, sy, spec0, spec1, orow, scr, stw, gs, gc); break;
+                case 16: rx_short_one<N, 16>(P, sy, spec0, spec1, orow, scr, stw, gs, gc); break;
+                case 32: rx_short_one<N, 32>(P, sy, spec0, spec1, orow, scr, stw, gs, gc); break;
+                case 64: rx_short_one<N, 64>(P, sy, spec0, spec1, orow, scr, stw, gs, gc); break;
+                case 128: rx_short_one<N, 128>(P, sy, spec0, spec1, orow, scr, stw, gs, gc); break;
+                case 256: rx_short_one<N, 256>(P, sy, spec0, spec1, orow, scr, stw, gs, gc); break;
+                case 512: rx_short_one<N, 512>(P, sy, spec0, spec1, orow, scr, stw, gs, gc); break;
+                case 1024: rx_short_one<N, 1024>(P, sy, spec0, spec1, orow, scr, stw, gs, gc); break;
                 default: break;
             }
         }
@@ -388,6 +411,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) tx_kernel(const KP
     float2* spec1 = sm + P.spec_stride;
     float2* carry = spec1 + P.spec_stride;
     float2* scr = carry + N / 2 + (threadIdx.x >> 5) * P.scratch_stride;
+    float2* stw = carry + N / 2 + kWarps * P.scratch_stride;  // W_{stab_len} for the short transforms
     constexpr int T = N / kPPT;
     const int tid = threadIdx.x;
     const bool act = tid < T;
@@ -396,11 +420,15 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) tx_kernel(const KP
     const int n1 = min(P.B, n0 + P.chunk);
     const float2* in_u = P.in + (long long)unit * P.in_stride;
     float2* out_u = P.out + (long long)unit * P.out_stride;
+    for (int i = tid; i < P.stab_len; i += kThreads) stw[i] = __ldg(&P.tw[i * (N / P.stab_len)]);
+    const int nfirst = n0 > 0 ? n0 - 1 : 0;
+    if (tid == 0) prefetch_l2(in_u + (long long)nfirst * P.row_len, 8LL * P.row_len);
 
-    for (int n = n0 > 0 ? n0 - 1 : 0; n < n1; ++n) {
+    for (int n = nfirst; n < n1; ++n) {
         const SymDev sy = P.sym[n];
         __syncthreads();  // previous symbol's transform no longer reads spec
-        tx_short_all<N, LU>(P, sy, in_u + (long long)n * P.row_len, spec0, spec1, scr);
+        if (tid == 0 && n + 1 < n1) prefetch_l2(in_u + (long long)(n + 1) * P.row_len, 8LL * P.row_len);
+        tx_short_all<N, LU>(P, sy, in_u + (long long)n * P.row_len, spec0, spec1, scr, stw);
         __syncthreads();
         // secondary contributions of shared transition bins, in rank order
         for (int l = 0; l < P.n_lvl; ++l) {
@@ -465,6 +493,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) rx_kernel(const KP
     float2* spec0 = sm;
     float2* spec1 = sm + P.spec_stride;
     float2* scr = spec1 + P.spec_stride + (threadIdx.x >> 5) * P.scratch_stride;
+    float2* stw = spec1 + P.spec_stride + kWarps * P.scratch_stride;
     constexpr int T = N / kPPT;
     const int tid = threadIdx.x;
     const bool act = tid < T;
@@ -473,9 +502,12 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) rx_kernel(const KP
     const int n1 = min(P.B, n0 + P.chunk);
     const float2* in_u = P.in + (long long)unit * P.in_stride;
     float2* out_u = P.out + (long long)unit * P.out_stride;
+    for (int i = tid; i < P.stab_len; i += kThreads) stw[i] = __ldg(&P.tw[i * (N / P.stab_len)]);
+    if (tid == 0) prefetch_l2(in_u + P.rx_base + P.sym[n0].sigma, 8LL * (3 * N / 2));
 
     for (int n = n0; n < n1; ++n) {
         const SymDev sy = P.sym[n];
+        if (tid == 0 && n + 1 < n1) prefetch_l2(in_u + P.rx_base + P.sym[n + 1].sigma, 8LL * (3 * N / 2));
         float2 v[2][kPPT];
         if (act) {
             // rx_segment (fc_sync.cpp:145-156): y0 = w[start, +N), y1 = w[start + N/2, +N)
@@ -501,7 +533,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) rx_kernel(const KP
             }
         }
         __syncthreads();
-        rx_short_all<N, LU>(P, sy, spec0, spec1, out_u + (long long)n * P.row_len, scr);
+        rx_short_all<N, LU>(P, sy, spec0, spec1, out_u + (long long)n * P.row_len, scr, stw);
     }
 }
 

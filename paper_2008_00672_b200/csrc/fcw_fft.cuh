@@ -158,9 +158,9 @@ FCW_DI int spad(int e) { return e + (e >> 4); }
 // tw is the plan table exp(-2 pi i m / N); e0 is already in table units and
 // k*e0 < N for every k < R.
 template <int R, int SIGN>
-FCW_DI void twiddle_powers(float2 (&w)[R], const float2* __restrict__ tw, int e0) {
+FCW_DI void twiddle_powers(float2 (&w)[R], const float2* tw, int e0) {
     auto ld = [&](int e) {
-        float2 v = __ldg(&tw[e]);
+        float2 v = tw[e];  // generic load: tw may live in SMEM or global
         if constexpr (SIGN > 0) v.y = -v.y;
         return v;
     };

@@ -49,6 +49,7 @@ struct KParams {
     int chunk, nchunks;
     int spec_stride;  // float2 per block spectrum in SMEM (>= N + n_ext, >= N + N/16)
     int scratch_stride;  // float2 per warp scratch
+    int stab_len;        // entries of the SMEM short-transform twiddle table (plan Lmax)
     int row_len;
     int grid_full;
     int fused;
@@ -63,7 +64,7 @@ struct KParams {
     const SubDev* sub;
     const SymDev* sym;
     const int* inv;      // [sum L] DFT bin -> active index or -1
-    const int4* bin;     // [sum L] per DFT bin b: {inv[b], dest[p0], bits(w[p0]), bits(w[p0]*bp1)}, p0 = b ^ L/2
+    const int2* bin;     // [sum L] per DFT bin b: {inv[b] | dest[p0] << 16, bits(w[p0])}, p0 = b ^ L/2
     const int* grp_sub;  // subband ids grouped by L
     const int* fix_tgt;  // [n_ext] target bin of each secondary contribution
     const int* zero_list;  // [n_zero] bins no subband touches
@@ -94,7 +95,7 @@ struct Plan {
     std::vector<SymDev> h_sym;
     std::vector<float> h_win;
     std::vector<int> h_inv, h_dest, h_grp_sub, h_fix, h_zero;
-    std::vector<int4> h_bin;
+    std::vector<int2> h_bin;
     int n_ext = 0, n_lvl = 0;
     std::vector<int> lvl_start;
     int n_groups = 0;
@@ -105,7 +106,7 @@ struct Plan {
     SubDev* d_sub = nullptr;
     SymDev* d_sym = nullptr;
     int *d_inv = nullptr, *d_grp_sub = nullptr, *d_fix = nullptr, *d_zero = nullptr;
-    int4* d_bin = nullptr;
+    int2* d_bin = nullptr;
     float2* d_tw = nullptr;
     // host-buffer pipeline state
     std::mutex host_mu;

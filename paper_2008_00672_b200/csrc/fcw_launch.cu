@@ -51,10 +51,12 @@ int scratch_stride(const Plan& p, int LU, bool rx_direct) {
     return two ? 2 * one : one;
 }
 
+int stab_len(const Plan& p) { return p.Lmax >= 64 ? p.Lmax : 0; }
+
 size_t smem_bytes(const Plan& p, bool tx, bool rx_direct) {
     const int LU = uniform_L(p);
     const size_t f2 = 2 * (size_t)spec_stride(p) + (tx ? p.N / 2 : 0) +
-                      (size_t)kWarps * scratch_stride(p, LU, rx_direct);
+                      (size_t)kWarps * scratch_stride(p, LU, rx_direct) + stab_len(p);
     return f2 * sizeof(float2);
 }
 
@@ -94,6 +96,7 @@ void fill_common(const Plan& p, KParams& kp) {
     kp.fix_tgt = p.d_fix;
     kp.zero_list = p.d_zero;
     kp.tw = p.d_tw;
+    kp.stab_len = stab_len(p);
 }
 
 size_t tx_smem_bytes(const Plan& p) { return smem_bytes(p, true, false); }
