@@ -80,12 +80,15 @@ FCW_DI float2 mul_jpow(float2 a) {
     if constexpr (k == 2) return make_float2(-a.x, -a.y);
     return make_float2(a.y, -a.x);
 }
+// j^k * a for a runtime k that differs across lanes: selects only, no branches
+// (a switch here diverges four ways inside a warp).
 FCW_DI float2 mul_jpow_rt(float2 a, int k) {
-    k &= 3;
-    if (k == 0) return a;
-    if (k == 1) return make_float2(-a.y, a.x);
-    if (k == 2) return make_float2(-a.x, -a.y);
-    return make_float2(a.y, -a.x);
+    const bool swap = k & 1;
+    const float sr = ((k + 1) & 2) ? -1.f : 1.f;  // k = 1, 2 negate the real part
+    const float si = (k & 2) ? -1.f : 1.f;        // k = 2, 3 negate the imaginary part
+    const float re = swap ? a.y : a.x;
+    const float im = swap ? a.x : a.y;
+    return make_float2(sr * re, si * im);
 }
 
 __host__ __device__ constexpr int cx_log2(int v) { return v <= 1 ? 0 : 1 + cx_log2(v / 2); }
@@ -105,18 +108,31 @@ FCW_DI void fft_stage(float2 (&x)[L]) {
             for (int s = 0; s < L; s += LEN) {
                 const float2 a = x[s + K];
                 const float2 b = x[s + K + H];
-                float2 wb;
-                if constexpr (K == 0) {
-                    wb = b;
-                } else if constexpr (4 * K == LEN) {
-                    wb = SIGN < 0 ? make_float2(b.y, -b.x) : make_float2(-b.y, b.x);
-                } else {
+                if constexpr (K == 0 || 4 * K == LEN) {
+                    // trivial twiddles 1 and -+j: 4 FADD
+                    const float2 wb = (K == 0) ? b : (SIGN < 0 ? make_float2(b.y, -b.x) : make_float2(-b.y, b.x));
+                    x[s + K] = cadd(a, wb);
+                    x[s + K + H] = csub(a, wb);
+                } else if constexpr (8 * K == LEN || 8 * K == 3 * LEN) {
+                    // +-45 degree twiddles: w*b = c*(b rotated), 2 FADD + 4 FFMA
                     constexpr float wr = Tw<LEN, K, SIGN>::re;
                     constexpr float wi = Tw<LEN, K, SIGN>::im;
-                    wb = make_float2(fmaf(b.x, wr, -b.y * wi), fmaf(b.x, wi, b.y * wr));
+                    constexpr float c = wr > 0.f ? wr : -wr;
+                    // w = c*(sr + j si) with sr, si in {+1,-1}
+                    constexpr float sr = wr > 0.f ? 1.f : -1.f, si = wi > 0.f ? 1.f : -1.f;
+                    const float tr = sr * b.x - si * b.y;
+                    const float ti = si * b.x + sr * b.y;
+                    x[s + K] = make_float2(fmaf(c, tr, a.x), fmaf(c, ti, a.y));
+                    x[s + K + H] = make_float2(fmaf(-c, tr, a.x), fmaf(-c, ti, a.y));
+                } else {
+                    // general twiddle: y0 = a + w b (4 FFMA), y1 = 2a - y0 (2 FFMA)
+                    constexpr float wr = Tw<LEN, K, SIGN>::re;
+                    constexpr float wi = Tw<LEN, K, SIGN>::im;
+                    const float y0r = fmaf(wr, b.x, fmaf(-wi, b.y, a.x));
+                    const float y0i = fmaf(wr, b.y, fmaf(wi, b.x, a.y));
+                    x[s + K] = make_float2(y0r, y0i);
+                    x[s + K + H] = make_float2(fmaf(2.f, a.x, -y0r), fmaf(2.f, a.y, -y0i));
                 }
-                x[s + K] = cadd(a, wb);
-                x[s + K + H] = csub(a, wb);
             }
             fft_stage<L, SIGN, LEN, K + 1>(x);
         } else {
