@@ -310,10 +310,11 @@ int fcw_plan_create(fcw_plan** out, int N, double overlap, const int* cp_high, i
     }
     p->row_active = act_off;
     p->row_full = full_off;
-    // secondary contributions: ext slots ordered by rank (level), then by order
-    std::stable_sort(secondary.begin(), secondary.end(),
-                     [](const Contrib& a, const Contrib& b) { return a.rank < b.rank; });
-    int max_rank = secondary.empty() ? 0 : secondary.back().rank;
+    // secondary contributions: ext slots numbered subband-major (a subband's
+    // secondary bins are consecutive from its ext_base); the fix-up list is
+    // ordered by contributor rank so shared bins are summed in a fixed order.
+    int max_rank = 0;
+    for (const Contrib& c : secondary) max_rank = std::max(max_rank, c.rank);
     if (N + (long long)secondary.size() >= 32768) {
         delete p;
         return fail(FCW_ENOTSUP, "too many shared transition bins for the 16-bit spectrum slot index");
@@ -324,15 +325,26 @@ int fcw_plan_create(fcw_plan** out, int N, double overlap, const int* cp_high, i
     }
     p->n_ext = (int)secondary.size();
     p->n_lvl = max_rank;
-    p->lvl_start.assign(max_rank + 1, 0);
+    std::vector<int> sec_idx(p->h_dest.size(), -1);
     for (int k = 0; k < p->n_ext; ++k) {
         const Contrib& c = secondary[k];
-        p->h_dest[p->h_sub[c.m].full_off + c.p0] = N + k;
-        p->h_fix.push_back(c.q);
+        fcw::SubDev& d = p->h_sub[c.m];
+        if (k == 0 || secondary[k - 1].m != c.m) d.ext_base = k;
+        p->h_dest[d.full_off + c.p0] = N + k;
+        sec_idx[d.full_off + c.p0] = k - d.ext_base;
     }
+    std::vector<int> order(p->n_ext);
+    for (int k = 0; k < p->n_ext; ++k) order[k] = k;
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int a, int b) { return secondary[a].rank < secondary[b].rank; });
+    for (int k : order) {
+        p->h_fix.push_back(secondary[k].q);
+        p->h_fix_slot.push_back(k);
+    }
+    p->lvl_start.assign(max_rank + 1, 0);
     for (int l = 0; l <= max_rank; ++l) {
         int k = 0;
-        while (k < p->n_ext && secondary[k].rank < l + 1) ++k;
+        while (k < p->n_ext && secondary[order[k]].rank < l + 1) ++k;
         p->lvl_start[l] = k;
     }
     for (int q = 0; q < N; ++q)
@@ -359,18 +371,36 @@ int fcw_plan_create(fcw_plan** out, int N, double overlap, const int* cp_high, i
         s.smodN = (int)mod_ll(cp_partial(p->cp, n), N);
         p->h_sym[n] = s;
     }
-    // packed per-bin table, indexed by DFT bin b (p0 = b ^ L/2)
-    p->h_bin.resize(p->h_inv.size());
-    for (int m = 0; m < M; ++m) {
-        const fcw::SubDev& d = p->h_sub[m];
-        for (int b = 0; b < d.L; ++b) {
-            const int p0 = b ^ (d.L / 2);
-            const float w = p->h_win[d.full_off + p0];
-            const int inv = p->h_inv[d.full_off + b], dest = p->h_dest[d.full_off + p0];
-            int2 e;
-            e.x = (inv & 0xffff) | (int)((unsigned)dest << 16);
-            std::memcpy(&e.y, &w, 4);
-            p->h_bin[d.full_off + b] = e;
+    // Bin-class table: per DFT bin b (p0 = b ^ L/2) the active index, the
+    // secondary-slot index relative to the subband's ext_base (-1 primary,
+    // -2 zero weight) and the window.  Subbands with identical rows share one
+    // class (regular allocations have 2-3 classes), so the table stays in L1.
+    {
+        std::map<std::vector<int>, int> classes;
+        for (int m = 0; m < M; ++m) {
+            fcw::SubDev& d = p->h_sub[m];
+            std::vector<int> key;
+            key.push_back(d.L);
+            std::vector<int2> rows(d.L);
+            for (int b = 0; b < d.L; ++b) {
+                const int p0 = b ^ (d.L / 2);
+                const float w = p->h_win[d.full_off + p0];
+                const int inv = p->h_inv[d.full_off + b];
+                const int dst = p->h_dest[d.full_off + p0];
+                const int sec = dst < 0 ? -2 : (dst >= N ? sec_idx[d.full_off + p0] : -1);
+                int2 e;
+                e.x = (inv & 0xffff) | (int)((unsigned)sec << 16);
+                std::memcpy(&e.y, &w, 4);
+                rows[b] = e;
+                key.push_back(e.x);
+                key.push_back(e.y);
+            }
+            auto it = classes.find(key);
+            if (it == classes.end()) {
+                it = classes.emplace(key, (int)p->h_cls.size()).first;
+                p->h_cls.insert(p->h_cls.end(), rows.begin(), rows.end());
+            }
+            d.cls_off = it->second;
         }
     }
     // device tables in one blob
@@ -386,7 +416,9 @@ int fcw_plan_create(fcw_plan** out, int N, double overlap, const int* cp_high, i
     const size_t o_sym = off;
     off = align(off + sizeof(fcw::SymDev) * B);
     const size_t o_bin = off;
-    off = align(off + sizeof(int2) * p->h_bin.size());
+    off = align(off + sizeof(int2) * p->h_cls.size());
+    const size_t o_fslot = off;
+    off = align(off + sizeof(int) * std::max<size_t>(1, p->h_fix_slot.size()));
     const size_t o_inv = off;
     off = align(off + sizeof(int) * p->h_inv.size());
     const size_t o_grp = off;
@@ -400,7 +432,9 @@ int fcw_plan_create(fcw_plan** out, int N, double overlap, const int* cp_high, i
     std::vector<unsigned char> host(off, 0);
     std::memcpy(&host[o_sub], p->h_sub.data(), sizeof(fcw::SubDev) * M);
     std::memcpy(&host[o_sym], p->h_sym.data(), sizeof(fcw::SymDev) * B);
-    std::memcpy(&host[o_bin], p->h_bin.data(), sizeof(int2) * p->h_bin.size());
+    std::memcpy(&host[o_bin], p->h_cls.data(), sizeof(int2) * p->h_cls.size());
+    if (!p->h_fix_slot.empty())
+        std::memcpy(&host[o_fslot], p->h_fix_slot.data(), sizeof(int) * p->h_fix_slot.size());
     std::memcpy(&host[o_inv], p->h_inv.data(), sizeof(int) * p->h_inv.size());
     std::memcpy(&host[o_grp], p->h_grp_sub.data(), sizeof(int) * p->h_grp_sub.size());
     if (!p->h_fix.empty()) std::memcpy(&host[o_fix], p->h_fix.data(), sizeof(int) * p->h_fix.size());
@@ -420,7 +454,8 @@ int fcw_plan_create(fcw_plan** out, int N, double overlap, const int* cp_high, i
     auto* base = static_cast<unsigned char*>(p->d_blob);
     p->d_sub = reinterpret_cast<fcw::SubDev*>(base + o_sub);
     p->d_sym = reinterpret_cast<fcw::SymDev*>(base + o_sym);
-    p->d_bin = reinterpret_cast<int2*>(base + o_bin);
+    p->d_cls = reinterpret_cast<int2*>(base + o_bin);
+    p->d_fix_slot = reinterpret_cast<int*>(base + o_fslot);
     p->d_inv = reinterpret_cast<int*>(base + o_inv);
     p->d_grp_sub = reinterpret_cast<int*>(base + o_grp);
     p->d_fix = reinterpret_cast<int*>(base + o_fix);

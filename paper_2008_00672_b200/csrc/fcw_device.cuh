@@ -31,16 +31,21 @@ namespace fcw {
 
 constexpr int kPPT = 16;  // long-transform points per thread and block
 
-// Bin-table entry (plan, per subband and DFT bin b), 8 bytes:
-//   x = (inv[b] & 0xffff) | dest[p0(b)] << 16  (active index / spectrum slot, -1 = none),
-//   y = bits(w[p0(b)]), with p0(b) = b ^ L/2.
+// Bin-class entry (plan, per class and DFT bin b), 8 bytes:
+//   x = (inv[b] & 0xffff) | sec(p0) << 16, y = bits(w[p0]), p0 = b ^ L/2;
+//   sec = -2: zero weight (no contribution), -1: primary (spectrum slot q),
+//   >= 0: extension slot N + ext_base + sec of a shared transition bin.
 struct Bin {
     int inv, dest;
     float w;
 };
+template <int N, int L>
 FCW_DI Bin bin_entry(const KParams& P, const SubDev& sd, int b) {
-    const int2 e = __ldg(&P.bin[sd.full_off + b]);
-    return Bin{(int)(short)(e.x & 0xffff), e.x >> 16, __int_as_float(e.y)};
+    const int2 e = __ldg(&P.cls[sd.cls_off + b]);
+    const int sec = e.x >> 16;
+    const int q = (sd.c - L / 2 + (b ^ (L / 2))) & (N - 1);
+    return Bin{(int)(short)(e.x & 0xffff), sec >= 0 ? N + sd.ext_base + sec : (sec == -1 ? q : -1),
+               __int_as_float(e.y)};
 }
 
 // Bulk L2 prefetch of [p, p + bytes) by one thread (cp.async.bulk, sm_90+):
@@ -87,7 +92,7 @@ FCW_DI void tx_short_thread(const KParams& P, const SymDev& sy, const float2* __
         float2 x[L];
         const float2 ph = cscale(tw_conj(P.tw, theta_exp<N>(sd.cmodN, sy.smodN)), sd.tx_scale);
 #pragma unroll
-        for (int b = 0; b < L; ++b) x[b] = cmul(grid_val(P, sd, row, b, bin_entry(P, sd, b).inv), ph);
+        for (int b = 0; b < L; ++b) x[b] = cmul(grid_val(P, sd, row, b, bin_entry<N, L>(P, sd, b).inv), ph);
         fft_reg<L, +1>(x);  // ofdm_modulate (scale folded into ph)
         const int lcp = sy.cp >> sd.logI;  // cp_truncate (fc_sync.cpp:26-32)
         float2 u0[L], u1[L];
@@ -103,7 +108,7 @@ FCW_DI void tx_short_thread(const KParams& P, const SymDev& sy, const float2* __
         fft_reg<L, -1>(u1);
 #pragma unroll
         for (int b = 0; b < L; ++b) {
-            const Bin e = bin_entry(P, sd, b);
+            const Bin e = bin_entry<N, L>(P, sd, b);
             if (e.dest >= 0) {
                 spec0[e.dest] = cscale(u0[b], e.w);
                 spec1[e.dest] = cscale(u1[b], e.w * sd.bp1);
@@ -129,7 +134,7 @@ FCW_DI void tx_short_warp(const KParams& P, const SymDev& sy, const float2* __re
         float2 v[1][PPT];
 #pragma unroll
         for (int k = 0; k < PPT; ++k) {
-            ent[k] = bin_entry(P, sd, lane + 32 * k);
+            ent[k] = bin_entry<N, L>(P, sd, lane + 32 * k);
             v[0][k] = cmul(grid_val(P, sd, row, lane + 32 * k, ent[k].inv), ph);
         }
         team_fft<L, 32, PPT, +1, 1, false>(v, b1, stw, sts, lane, true);
@@ -218,7 +223,7 @@ FCW_DI void rx_short_thread(const KParams& P, const SymDev& sy, const float2* sp
         float2 g0[L], g1[L];
 #pragma unroll
         for (int b = 0; b < L; ++b) {
-            const float w = bin_entry(P, sd, b).w;
+            const float w = bin_entry<N, L>(P, sd, b).w;
             const int q = (sd.c - L / 2 + (b ^ (L / 2))) & (N - 1);
             g0[b] = cscale(spec0[q], w);
             g1[b] = cscale(spec1[q], w * sd.bp1);
@@ -274,7 +279,7 @@ FCW_DI void rx_short_thread(const KParams& P, const SymDev& sy, const float2* sp
             if (P.grid_full) {
                 orow[sd.full_off + b] = g0[b];
             } else {
-                const int a = bin_entry(P, sd, b).inv;
+                const int a = bin_entry<N, L>(P, sd, b).inv;
                 if (a >= 0) orow[sd.act_off + a] = g0[b];
             }
         }
@@ -296,7 +301,7 @@ FCW_DI void rx_short_warp(const KParams& P, const SymDev& sy, const float2* spec
 #pragma unroll
         for (int k = 0; k < PPT; ++k) {
             const int b = lane + 32 * k;
-            const Bin e = bin_entry(P, sd, b);
+            const Bin e = bin_entry<N, L>(P, sd, b);
             inv[k] = e.inv;
             const int q = (sd.c - L / 2 + (b ^ (L / 2))) & (N - 1);
             g0[0][k] = cscale(spec0[q], e.w);
@@ -433,9 +438,9 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) tx_kernel(const KP
         // secondary contributions of shared transition bins, in rank order
         for (int l = 0; l < P.n_lvl; ++l) {
             for (int k = P.lvl_start[l] + tid; k < P.lvl_start[l + 1]; k += kThreads) {
-                const int q = __ldg(&P.fix_tgt[k]);
-                spec0[q] = cadd(spec0[q], spec0[N + k]);
-                spec1[q] = cadd(spec1[q], spec1[N + k]);
+                const int q = __ldg(&P.fix_tgt[k]), e = N + __ldg(&P.fix_slot[k]);
+                spec0[q] = cadd(spec0[q], spec0[e]);
+                spec1[q] = cadd(spec1[q], spec1[e]);
             }
             __syncthreads();
         }

@@ -30,7 +30,9 @@ struct SubDev {
     float bp1;     // block_phase(1, c, L/2, L) = +-1 (fc_core.cpp:41-44, lambda = 1/2)
     float tx_scale;  // sqrt(I) / (N sqrt(L)): folds ofdm_modulate sqrt(L)/L, IDFT_N 1/N, tx_symbol sqrt(I)
     float rx_s0;     // sqrt(I) (L/N) / sqrt(L)  (fc_sync.cpp:238-240)
-    float pad_;
+    int cls_off;     // offset of this subband's bin-class row in the class table
+    int ext_base;    // first extension slot of this subband's secondary bins
+    int pad_[3];
 };
 
 // Per-symbol geometry (all integer-exact on the host).
@@ -64,9 +66,10 @@ struct KParams {
     const SubDev* sub;
     const SymDev* sym;
     const int* inv;      // [sum L] DFT bin -> active index or -1
-    const int2* bin;     // [sum L] per DFT bin b: {inv[b] | dest[p0] << 16, bits(w[p0])}, p0 = b ^ L/2
+    const int2* cls;     // bin-class rows: per DFT bin b {inv[b] | sec(p0) << 16, bits(w[p0])}, p0 = b ^ L/2
     const int* grp_sub;  // subband ids grouped by L
-    const int* fix_tgt;  // [n_ext] target bin of each secondary contribution
+    const int* fix_tgt;  // [n_ext] target bin of each secondary contribution, rank-ordered
+    const int* fix_slot; // [n_ext] its extension slot
     const int* zero_list;  // [n_zero] bins no subband touches
     const float2* tw;    // [N] exp(-2 pi i k / N)
     const float2* in;
@@ -95,7 +98,8 @@ struct Plan {
     std::vector<SymDev> h_sym;
     std::vector<float> h_win;
     std::vector<int> h_inv, h_dest, h_grp_sub, h_fix, h_zero;
-    std::vector<int2> h_bin;
+    std::vector<int2> h_cls;
+    std::vector<int> h_fix_slot;
     int n_ext = 0, n_lvl = 0;
     std::vector<int> lvl_start;
     int n_groups = 0;
@@ -106,7 +110,8 @@ struct Plan {
     SubDev* d_sub = nullptr;
     SymDev* d_sym = nullptr;
     int *d_inv = nullptr, *d_grp_sub = nullptr, *d_fix = nullptr, *d_zero = nullptr;
-    int2* d_bin = nullptr;
+    int2* d_cls = nullptr;
+    int* d_fix_slot = nullptr;
     float2* d_tw = nullptr;
     // host-buffer pipeline state
     std::mutex host_mu;

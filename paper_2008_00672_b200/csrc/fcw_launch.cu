@@ -90,7 +90,8 @@ void fill_common(const Plan& p, KParams& kp) {
     kp.sub = p.d_sub;
     kp.sym = p.d_sym;
     kp.inv = p.d_inv;
-    kp.bin = p.d_bin;
+    kp.cls = p.d_cls;
+    kp.fix_slot = p.d_fix_slot;
     // uniform-L plans iterate subbands directly (identity group order)
     kp.grp_sub = uniform_L(p) ? nullptr : p.d_grp_sub;
     kp.fix_tgt = p.d_fix;
