@@ -70,19 +70,25 @@ long long cp_partial(const std::vector<int>& cp, int n) {
     return s;
 }
 
-int pick_chunk(const fcw::Plan& p, int S) {
+// Symbols per work item.  Items are handed out dynamically to the resident
+// CTAs (~2 per SM); aim for ~16 items per CTA on TX (each item recomputes one
+// symbol to obtain its incoming carry) and ~32 on RX (no recompute).
+int pick_chunk(const fcw::Plan& p, int S, bool tx) {
+    if (const char* e = std::getenv(tx ? "FCW_CHUNK_TX" : "FCW_CHUNK_RX")) {
+        const int c = std::atoi(e);
+        if (c > 0) return std::min(c, p.B);
+    }
     if (const char* e = std::getenv("FCW_CHUNK")) {
         const int c = std::atoi(e);
         if (c > 0) return std::min(c, p.B);
     }
-    // enough CTAs for ~16 waves at one CTA per SM, but long enough runs to
-    // amortise the one recomputed symbol per TX chunk
-    const long long target = 16LL * 148;
-    long long per_unit = (target + S - 1) / std::max(S, 1);
-    if (per_unit < 1) per_unit = 1;
-    int chunk = (int)((p.B + per_unit - 1) / per_unit);
-    chunk = std::max(chunk, std::min(p.B, 8));
-    return std::min(chunk, p.B);
+    const long long resident = 2LL * 148;
+    const long long per_cta = tx ? 16 : 32;
+    long long c = ((long long)p.B * std::max(S, 1) + per_cta * resident - 1) / (per_cta * resident);
+    c = std::max<long long>(c, tx ? std::min(p.B, 8) : 1);
+    c = std::min<long long>(c, p.B);
+    const long long nch = (p.B + c - 1) / c;  // rebalance run lengths
+    return (int)((p.B + nch - 1) / nch);
 }
 
 }  // namespace
@@ -470,7 +476,7 @@ int fcw_plan_create(fcw_plan** out, int N, double overlap, const int* cp_high, i
         delete p;
         return fail(FCW_ENOTSUP, "plan exceeds the per-CTA shared-memory envelope");
     }
-    p->chunk = pick_chunk(*p, 1);
+    p->chunk = pick_chunk(*p, 1, true);
     *out = p;
     return FCW_OK;
 }
@@ -564,7 +570,7 @@ int fcw_tx(const fcw_plan* p, const void* grid, int64_t grid_stride, void* wave,
     if (wave_stride < p->Q) return fail(FCW_EINVAL, "waveform unit stride smaller than Q");
     fcw::KParams kp{};
     fcw::fill_common(*p, kp);
-    kp.chunk = pick_chunk(*p, S);
+    kp.chunk = pick_chunk(*p, S, true);
     kp.nchunks = (p->B + kp.chunk - 1) / kp.chunk;
     kp.row_len = row;
     kp.grid_full = (flags & FCW_GRID_FULL) ? 1 : 0;
@@ -596,7 +602,7 @@ int fcw_rx(const fcw_plan* p, const void* wave, int64_t wave_stride, int64_t wav
     if (grid_stride < (int64_t)p->B * row) return fail(FCW_EINVAL, "grid unit stride too small");
     fcw::KParams kp{};
     fcw::fill_common(*p, kp);
-    kp.chunk = pick_chunk(*p, S);
+    kp.chunk = pick_chunk(*p, S, false);
     kp.nchunks = (p->B + kp.chunk - 1) / kp.chunk;
     kp.row_len = row;
     kp.grid_full = (flags & FCW_GRID_FULL) ? 1 : 0;

@@ -48,6 +48,33 @@ FCW_DI Bin bin_entry(const KParams& P, const SubDev& sd, int b) {
                __int_as_float(e.y)};
 }
 
+// Decoded class entry for warp-path lane element b = lane + 32k (L >= 64):
+// flipping bit L/2 of b only touches k, so the primary slot is qbase + 32 k'.
+template <int I>
+struct IC {
+    static constexpr int value = I;
+};
+template <int Nn, int I = 0, class F>
+FCW_DI void static_for(F&& f) {
+    if constexpr (I < Nn) {
+        f(IC<I>{});
+        static_for<Nn, I + 1>(f);
+    }
+}
+
+struct BinW {
+    int inv;   // active index or -1
+    int dest;  // spectrum slot or -1
+    float w;
+};
+template <int N, int L, int K>
+FCW_DI BinW bin_warp(const int2 e, int qbase, int ext0) {
+    constexpr int KP = K ^ (L / 64);  // (lane + 32K) ^ (L/2) == lane + 32*KP
+    const int sec = e.x >> 16;
+    const int q = (qbase + 32 * KP) & (N - 1);
+    return BinW{(int)(short)(e.x & 0xffff), sec >= 0 ? ext0 + sec : (sec == -1 ? q : -1), __int_as_float(e.y)};
+}
+
 // Bulk L2 prefetch of [p, p + bytes) by one thread (cp.async.bulk, sm_90+):
 // the next symbol's input is on its way from HBM while this one computes.
 FCW_DI void prefetch_l2(const void* p, long long bytes) {
@@ -130,16 +157,27 @@ FCW_DI void tx_short_warp(const KParams& P, const SymDev& sy, const float2* __re
         const int m = P.grp_sub ? __ldg(&P.grp_sub[gstart + i]) : gstart + i;
         const SubDev sd = P.sub[m];
         const float2 ph = cscale(tw_conj(P.tw, theta_exp<N>(sd.cmodN, sy.smodN)), sd.tx_scale);
-        Bin ent[PPT];
-        float2 v[1][PPT];
+        const int2* ce = P.cls + sd.cls_off + lane;
+        const int qbase = sd.c - L / 2 + lane, ext0 = N + sd.ext_base;
+        int2 ent[PPT];
 #pragma unroll
-        for (int k = 0; k < PPT; ++k) {
-            ent[k] = bin_entry<N, L>(P, sd, lane + 32 * k);
-            v[0][k] = cmul(grid_val(P, sd, row, lane + 32 * k, ent[k].inv), ph);
+        for (int k = 0; k < PPT; ++k) ent[k] = __ldg(&ce[32 * k]);
+        float2 v[1][PPT];
+        if (P.grid_full) {
+            const float2* g = row + sd.full_off + lane;
+#pragma unroll
+            for (int k = 0; k < PPT; ++k) v[0][k] = cmul(g[32 * k], ph);
+        } else {
+            const float2* g = row + sd.act_off;
+#pragma unroll
+            for (int k = 0; k < PPT; ++k) {
+                const int inv = (int)(short)(ent[k].x & 0xffff);
+                v[0][k] = inv >= 0 ? cmul(g[inv], ph) : zero2();
+            }
         }
         team_fft<L, 32, PPT, +1, 1, false>(v, b1, stw, sts, lane, true);
         const int lcp = sy.cp >> sd.logI;
-        float2 u0[1][PPT], u1[1][PPT];
+        float2 uu[2][PPT];  // block-0 / block-1 DFT inputs
         if constexpr (L >= 128) {
             // L/4 is a multiple of 32: the circular shifts are register renames
 #pragma unroll
@@ -147,8 +185,8 @@ FCW_DI void tx_short_warp(const KParams& P, const SymDev& sy, const float2* __re
                 const int e = lane + 32 * k;
                 const bool in0 = (e >= L / 4 - lcp) && (e < 3 * L / 4);
                 const bool in1 = (e >= L / 4) && (e < 3 * L / 4);
-                u0[0][k] = in0 ? v[0][(k - PPT / 4 + PPT) % PPT] : zero2();
-                u1[0][k] = in1 ? v[0][(k + PPT / 4) % PPT] : zero2();
+                uu[0][k] = in0 ? v[0][(k - PPT / 4 + PPT) % PPT] : zero2();
+                uu[1][k] = in1 ? v[0][(k + PPT / 4) % PPT] : zero2();
             }
         } else {
             __syncwarp();
@@ -160,18 +198,25 @@ FCW_DI void tx_short_warp(const KParams& P, const SymDev& sy, const float2* __re
                 const int e = lane + 32 * k;
                 const bool in0 = (e >= L / 4 - lcp) && (e < 3 * L / 4);
                 const bool in1 = (e >= L / 4) && (e < 3 * L / 4);
-                u0[0][k] = in0 ? scr[(e - L / 4) & (L - 1)] : zero2();
-                u1[0][k] = in1 ? scr[(e + L / 4) & (L - 1)] : zero2();
+                uu[0][k] = in0 ? scr[(e - L / 4) & (L - 1)] : zero2();
+                uu[1][k] = in1 ? scr[(e + L / 4) & (L - 1)] : zero2();
             }
         }
-        team_fft<L, 32, PPT, -1, 1, false>(u0, b1, stw, sts, lane, true);
-#pragma unroll
-        for (int k = 0; k < PPT; ++k)
-            if (ent[k].dest >= 0) spec0[ent[k].dest] = cscale(u0[0][k], ent[k].w);
-        team_fft<L, 32, PPT, -1, 1, false>(u1, b1, stw, sts, lane, true);
-#pragma unroll
-        for (int k = 0; k < PPT; ++k)
-            if (ent[k].dest >= 0) spec1[ent[k].dest] = cscale(u1[0][k], ent[k].w * sd.bp1);
+        {
+            // both block DFTs in lockstep: shared twiddles, twice the ILP
+            float2* const b2[2] = {scr, scr + P.scratch_stride / 2};
+            team_fft<L, 32, PPT, -1, 2, false>(uu, b2, stw, sts, lane, true);
+        }
+        const float bp1 = sd.bp1;
+        auto scatter = [&](auto kc) {
+            constexpr int K = decltype(kc)::value;
+            const BinW e = bin_warp<N, L, K>(ent[K], qbase, ext0);
+            if (e.dest >= 0) {
+                spec0[e.dest] = cscale(uu[0][K], e.w);
+                spec1[e.dest] = cscale(uu[1][K], e.w * bp1);
+            }
+        };
+        static_for<PPT>(scatter);
     }
 }
 
@@ -298,14 +343,20 @@ FCW_DI void rx_short_warp(const KParams& P, const SymDev& sy, const float2* spec
         const SubDev sd = P.sub[m];
         float2 g0[1][PPT], g1[1][PPT];
         int inv[PPT];
-#pragma unroll
-        for (int k = 0; k < PPT; ++k) {
-            const int b = lane + 32 * k;
-            const Bin e = bin_entry<N, L>(P, sd, b);
-            inv[k] = e.inv;
-            const int q = (sd.c - L / 2 + (b ^ (L / 2))) & (N - 1);
-            g0[0][k] = cscale(spec0[q], e.w);
-            g1[0][k] = cscale(spec1[q], e.w * sd.bp1);
+        {
+            const int2* ce = P.cls + sd.cls_off + lane;
+            const int qbase = sd.c - L / 2 + lane;
+            const float bp1 = sd.bp1;
+            static_for<PPT>([&](auto kc) {
+                constexpr int K = decltype(kc)::value;
+                constexpr int KP = K ^ (L / 64);  // (lane + 32K) ^ (L/2) == lane + 32*KP
+                const int2 e = __ldg(&ce[32 * K]);
+                inv[K] = (int)(short)(e.x & 0xffff);
+                const float w = __int_as_float(e.y);
+                const int q = (qbase + 32 * KP) & (N - 1);
+                g0[0][K] = cscale(spec0[q], w);
+                g1[0][K] = cscale(spec1[q], w * bp1);
+            });
         }
         const float2 ph = __ldg(&P.tw[theta_exp<N>(sd.cmodN, sy.smodN)]);
         if (P.fused) {
@@ -354,13 +405,15 @@ FCW_DI void rx_short_warp(const KParams& P, const SymDev& sy, const float2* spec
 #pragma unroll
             for (int k = 0; k < PPT; ++k) g0[0][k] = cmul(x[0][k], phs);
         }
+        if (P.grid_full) {
+            float2* o = orow + sd.full_off + lane;
 #pragma unroll
-        for (int k = 0; k < PPT; ++k) {
-            const int b = lane + 32 * k;
-            if (P.grid_full)
-                orow[sd.full_off + b] = g0[0][k];
-            else if (inv[k] >= 0)
-                orow[sd.act_off + inv[k]] = g0[0][k];
+            for (int k = 0; k < PPT; ++k) o[32 * k] = g0[0][k];
+        } else {
+            float2* o = orow + sd.act_off;
+#pragma unroll
+            for (int k = 0; k < PPT; ++k)
+                if (inv[k] >= 0) o[inv[k]] = g0[0][k];
         }
         __syncwarp();
     }
@@ -408,83 +461,99 @@ constexpr int min_blocks() {
     return (LU >= 64 || (LU > 0 && LU <= 16)) ? 2 : 1;
 }
 
+// Next work item (unit, run of symbols) for this persistent CTA: dynamic
+// scheduling through one global counter keeps the tail short.
+FCW_DI int next_item(const KParams& P, int* s_item) {
+    __syncthreads();  // everyone has read the previous item id
+    if (threadIdx.x == 0) *s_item = atomicAdd(P.item_counter, 1);
+    __syncthreads();
+    return *s_item;
+}
+
 template <int N, int LU>
 __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) tx_kernel(const KParams P) {
     extern __shared__ float4 smem_raw[];
     float2* sm = reinterpret_cast<float2*>(smem_raw);
     float2* spec0 = sm;
     float2* spec1 = sm + P.spec_stride;
-    float2* carry = spec1 + P.spec_stride;
-    float2* scr = carry + N / 2 + (threadIdx.x >> 5) * P.scratch_stride;
-    float2* stw = carry + N / 2 + kWarps * P.scratch_stride;  // W_{stab_len} for the short transforms
+    float2* scr = spec1 + P.spec_stride + (threadIdx.x >> 5) * P.scratch_stride;
+    float2* stw = spec1 + P.spec_stride + kWarps * P.scratch_stride;  // W_{stab_len} for the short transforms
+    int* s_item = reinterpret_cast<int*>(stw + P.stab_len);
+    // The block-1 tail that overlaps the next symbol lives in a per-CTA global
+    // (L2-resident) buffer: written and read back by this CTA only.
+    float2* carry = P.carry + (long long)blockIdx.x * (N / 2);
     constexpr int T = N / kPPT;
     const int tid = threadIdx.x;
     const bool act = tid < T;
-    const int unit = blockIdx.x / P.nchunks;
-    const int n0 = (blockIdx.x % P.nchunks) * P.chunk;
-    const int n1 = min(P.B, n0 + P.chunk);
-    const float2* in_u = P.in + (long long)unit * P.in_stride;
-    float2* out_u = P.out + (long long)unit * P.out_stride;
     for (int i = tid; i < P.stab_len; i += kThreads) stw[i] = __ldg(&P.tw[i * (N / P.stab_len)]);
-    const int nfirst = n0 > 0 ? n0 - 1 : 0;
-    if (tid == 0) prefetch_l2(in_u + (long long)nfirst * P.row_len, 8LL * P.row_len);
 
-    for (int n = nfirst; n < n1; ++n) {
-        const SymDev sy = P.sym[n];
-        __syncthreads();  // previous symbol's transform no longer reads spec
-        if (tid == 0 && n + 1 < n1) prefetch_l2(in_u + (long long)(n + 1) * P.row_len, 8LL * P.row_len);
-        tx_short_all<N, LU>(P, sy, in_u + (long long)n * P.row_len, spec0, spec1, scr, stw);
-        __syncthreads();
-        // secondary contributions of shared transition bins, in rank order
-        for (int l = 0; l < P.n_lvl; ++l) {
-            for (int k = P.lvl_start[l] + tid; k < P.lvl_start[l + 1]; k += kThreads) {
-                const int q = __ldg(&P.fix_tgt[k]), e = N + __ldg(&P.fix_slot[k]);
-                spec0[q] = cadd(spec0[q], spec0[e]);
-                spec1[q] = cadd(spec1[q], spec1[e]);
+    for (int item = next_item(P, s_item); item < P.n_items; item = next_item(P, s_item)) {
+        const int unit = item / P.nchunks;
+        const int n0 = (item % P.nchunks) * P.chunk;
+        const int n1 = min(P.B, n0 + P.chunk);
+        const float2* in_u = P.in + (long long)unit * P.in_stride;
+        float2* out_u = P.out + (long long)unit * P.out_stride;
+        const int nfirst = n0 > 0 ? n0 - 1 : 0;
+        if (tid == 0) prefetch_l2(in_u + (long long)nfirst * P.row_len, 8LL * P.row_len);
+
+        for (int n = nfirst; n < n1; ++n) {
+            const SymDev sy = P.sym[n];
+            __syncthreads();  // previous symbol's transform no longer reads spec
+            if (tid == 0 && n + 1 < n1) prefetch_l2(in_u + (long long)(n + 1) * P.row_len, 8LL * P.row_len);
+            if (!(P.dbg_skip & 1))
+                tx_short_all<N, LU>(P, sy, in_u + (long long)n * P.row_len, spec0, spec1, scr, stw);
+            __syncthreads();
+            // secondary contributions of shared transition bins, in rank order
+            for (int l = 0; l < P.n_lvl; ++l) {
+                for (int k = P.lvl_start[l] + tid; k < P.lvl_start[l + 1]; k += kThreads) {
+                    const int q = __ldg(&P.fix_tgt[k]), e = N + __ldg(&P.fix_slot[k]);
+                    spec0[q] = cadd(spec0[q], spec0[e]);
+                    spec1[q] = cadd(spec1[q], spec1[e]);
+                }
+                __syncthreads();
+            }
+            for (int k = tid; k < P.n_zero; k += kThreads) {
+                const int q = __ldg(&P.zero_list[k]);
+                spec0[q] = zero2();
+                spec1[q] = zero2();
             }
             __syncthreads();
-        }
-        for (int k = tid; k < P.n_zero; k += kThreads) {
-            const int q = __ldg(&P.zero_list[k]);
-            spec0[q] = zero2();
-            spec1[q] = zero2();
-        }
-        __syncthreads();
 
-        float2 cr[8];
+            float2 cr[8];
 #pragma unroll
-        for (int m = 0; m < 8; ++m) {
-            const int u = tid + T * m;
-            cr[m] = (act && u < sy.carry_len) ? carry[u] : zero2();
-        }
-        float2 v[2][kPPT];
-        if (act) {
-#pragma unroll
-            for (int m = 0; m < kPPT; ++m) {
-                v[0][m] = spec0[tid + T * m];
-                v[1][m] = spec1[tid + T * m];
+            for (int m = 0; m < 8; ++m) {
+                const int u = tid + T * m;
+                cr[m] = (act && n > nfirst && u < sy.carry_len) ? carry[u] : zero2();
             }
-        }
-        {
-            float2* const bufs[2] = {spec0, spec1};
-            team_fft<N, T, kPPT, +1, 2, true>(v, bufs, P.tw, 1, tid, act);
-        }
-        if constexpr (T == 1) __syncthreads();
-        // symbol-wise overlap-add: block 0 at 0, block 1 at N/2, carry from n-1
-        if (act) {
-            const bool emit = n >= n0;
-            float2* dst = out_u + sy.sigma;
+            float2 v[2][kPPT];
+            if (act) {
 #pragma unroll
-            for (int mm = 0; mm < 24; ++mm) {
-                const int u = tid + T * mm;
-                float2 val = zero2();
-                if (mm < 16) val = v[0][mm];
-                if (mm >= 8) val = cadd(val, v[1][mm - 8]);
-                if (mm < 8) val = cadd(val, cr[mm]);
-                if (u < sy.own_len) {
-                    if (emit) dst[u] = val;
-                } else {
-                    carry[u - sy.own_len] = val;
+                for (int m = 0; m < kPPT; ++m) {
+                    v[0][m] = spec0[tid + T * m];
+                    v[1][m] = spec1[tid + T * m];
+                }
+            }
+            {
+                float2* const bufs[2] = {spec0, spec1};
+                if (!(P.dbg_skip & 2)) team_fft<N, T, kPPT, +1, 2, true>(v, bufs, P.tw, 1, tid, act);
+            }
+            __syncthreads();  // every thread has read its carry before it is overwritten
+            // symbol-wise overlap-add: block 0 at 0, block 1 at N/2, carry from n-1
+            if (act) {
+                const bool emit = n >= n0;
+                float2* dst = out_u + sy.sigma;
+#pragma unroll
+                for (int mm = 0; mm < 24; ++mm) {
+                    const int u = tid + T * mm;
+                    float2 val = zero2();
+                    if (mm < 16) val = v[0][mm];
+                    if (mm >= 8) val = cadd(val, v[1][mm - 8]);
+                    if (mm < 8) val = cadd(val, cr[mm]);
+                    if (u < sy.own_len) {
+                        if (emit) dst[u] = val;
+                    } else {
+                        carry[u - sy.own_len] = val;
+                    }
                 }
             }
         }
@@ -499,46 +568,51 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) rx_kernel(const KP
     float2* spec1 = sm + P.spec_stride;
     float2* scr = spec1 + P.spec_stride + (threadIdx.x >> 5) * P.scratch_stride;
     float2* stw = spec1 + P.spec_stride + kWarps * P.scratch_stride;
+    int* s_item = reinterpret_cast<int*>(stw + P.stab_len);
     constexpr int T = N / kPPT;
     const int tid = threadIdx.x;
     const bool act = tid < T;
-    const int unit = blockIdx.x / P.nchunks;
-    const int n0 = (blockIdx.x % P.nchunks) * P.chunk;
-    const int n1 = min(P.B, n0 + P.chunk);
-    const float2* in_u = P.in + (long long)unit * P.in_stride;
-    float2* out_u = P.out + (long long)unit * P.out_stride;
     for (int i = tid; i < P.stab_len; i += kThreads) stw[i] = __ldg(&P.tw[i * (N / P.stab_len)]);
-    if (tid == 0) prefetch_l2(in_u + P.rx_base + P.sym[n0].sigma, 8LL * (3 * N / 2));
 
-    for (int n = n0; n < n1; ++n) {
-        const SymDev sy = P.sym[n];
-        if (tid == 0 && n + 1 < n1) prefetch_l2(in_u + P.rx_base + P.sym[n + 1].sigma, 8LL * (3 * N / 2));
-        float2 v[2][kPPT];
-        if (act) {
-            // rx_segment (fc_sync.cpp:145-156): y0 = w[start, +N), y1 = w[start + N/2, +N)
-            const float2* src = in_u + P.rx_base + sy.sigma + tid;
+    for (int item = next_item(P, s_item); item < P.n_items; item = next_item(P, s_item)) {
+        const int unit = item / P.nchunks;
+        const int n0 = (item % P.nchunks) * P.chunk;
+        const int n1 = min(P.B, n0 + P.chunk);
+        const float2* in_u = P.in + (long long)unit * P.in_stride;
+        float2* out_u = P.out + (long long)unit * P.out_stride;
+        if (tid == 0) prefetch_l2(in_u + P.rx_base + P.sym[n0].sigma, 8LL * (3 * N / 2));
+
+        for (int n = n0; n < n1; ++n) {
+            const SymDev sy = P.sym[n];
+            if (tid == 0 && n + 1 < n1) prefetch_l2(in_u + P.rx_base + P.sym[n + 1].sigma, 8LL * (3 * N / 2));
+            float2 v[2][kPPT];
+            if (act) {
+                // rx_segment (fc_sync.cpp:145-156): y0 = w[start, +N), y1 = w[start + N/2, +N)
+                const float2* src = in_u + P.rx_base + sy.sigma + tid;
 #pragma unroll
-            for (int mm = 0; mm < 24; ++mm) {
-                const float2 val = __ldg(&src[T * mm]);
-                if (mm < 16) v[0][mm] = val;
-                if (mm >= 8) v[1][mm - 8] = val;
+                for (int mm = 0; mm < 24; ++mm) {
+                    const float2 val = __ldg(&src[T * mm]);
+                    if (mm < 16) v[0][mm] = val;
+                    if (mm >= 8) v[1][mm - 8] = val;
+                }
             }
-        }
-        __syncthreads();  // previous symbol's subband stage no longer reads spec
-        {
-            float2* const bufs[2] = {spec0, spec1};
-            team_fft<N, T, kPPT, -1, 2, true>(v, bufs, P.tw, 1, tid, act);
-        }
-        __syncthreads();
-        if (act) {
+            __syncthreads();  // previous symbol's subband stage no longer reads spec
+            {
+                float2* const bufs[2] = {spec0, spec1};
+                if (!(P.dbg_skip & 2)) team_fft<N, T, kPPT, -1, 2, true>(v, bufs, P.tw, 1, tid, act);
+            }
+            __syncthreads();
+            if (act) {
 #pragma unroll
-            for (int m = 0; m < kPPT; ++m) {
-                spec0[tid + T * m] = v[0][m];
-                spec1[tid + T * m] = v[1][m];
+                for (int m = 0; m < kPPT; ++m) {
+                    spec0[tid + T * m] = v[0][m];
+                    spec1[tid + T * m] = v[1][m];
+                }
             }
+            __syncthreads();
+            if (!(P.dbg_skip & 1))
+                rx_short_all<N, LU>(P, sy, spec0, spec1, out_u + (long long)n * P.row_len, scr, stw);
         }
-        __syncthreads();
-        rx_short_all<N, LU>(P, sy, spec0, spec1, out_u + (long long)n * P.row_len, scr, stw);
     }
 }
 

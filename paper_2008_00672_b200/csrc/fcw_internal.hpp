@@ -49,12 +49,14 @@ struct SymDev {
 struct KParams {
     int N, B, M;
     int chunk, nchunks;
+    int n_items;         // S * nchunks work items, handed out through item_counter
     int spec_stride;  // float2 per block spectrum in SMEM (>= N + n_ext, >= N + N/16)
     int scratch_stride;  // float2 per warp scratch
     int stab_len;        // entries of the SMEM short-transform twiddle table (plan Lmax)
     int row_len;
     int grid_full;
     int fused;
+    int dbg_skip;        // dev-only timing knob (FCW_DEBUG_SKIP): 1 = short stage, 2 = long transform
     int n_ext, n_zero, n_lvl;
     int lvl_start[kMaxLevels + 1];
     int n_groups;
@@ -74,6 +76,8 @@ struct KParams {
     const float2* tw;    // [N] exp(-2 pi i k / N)
     const float2* in;
     float2* out;
+    int* item_counter;   // per-launch scratch: dynamic work counter
+    float2* carry;       // per-launch scratch: gridDim.x * N/2 TX carry buffers
 };
 
 struct Plan {

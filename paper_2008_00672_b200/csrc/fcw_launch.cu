@@ -1,4 +1,7 @@
 // Launch configuration and the K-GEN generator kernel.
+#include <algorithm>
+#include <cstdlib>
+
 #include "fcw_device.cuh"
 
 namespace fcw {
@@ -43,11 +46,11 @@ int spec_stride(const Plan& p) {
 }
 
 // Warp scratch: one padded buffer of the largest warp-path L, two where a path
-// needs both blocks' short outputs at once (direct RX at L = 64, generic).
-int scratch_stride(const Plan& p, int LU, bool rx_direct) {
+// transforms both blocks at once (TX; direct RX at L = 64 and generic plans).
+int scratch_stride(const Plan& p, int LU, bool tx, bool rx_direct) {
     if (p.Lmax < 64) return 0;
     const int one = (p.Lmax + p.Lmax / 16 + 2 + 1) & ~1;
-    const bool two = rx_direct && (LU == 0 || LU == 64 || p.Lmax == 64);
+    const bool two = tx || (rx_direct && (LU == 0 || LU == 64 || p.Lmax == 64));
     return two ? 2 * one : one;
 }
 
@@ -55,18 +58,39 @@ int stab_len(const Plan& p) { return p.Lmax >= 64 ? p.Lmax : 0; }
 
 size_t smem_bytes(const Plan& p, bool tx, bool rx_direct) {
     const int LU = uniform_L(p);
-    const size_t f2 = 2 * (size_t)spec_stride(p) + (tx ? p.N / 2 : 0) +
-                      (size_t)kWarps * scratch_stride(p, LU, rx_direct) + stab_len(p);
+    const size_t f2 = 2 * (size_t)spec_stride(p) + (size_t)kWarps * scratch_stride(p, LU, tx, rx_direct) +
+                      stab_len(p) + 1 /* s_item */;
     return f2 * sizeof(float2);
 }
 
-cudaError_t launch_one(KernelFn k, size_t smem, int grid, const KParams& kp, cudaStream_t st) {
+// Persistent launch: as many CTAs as can be resident, each pulling work items
+// (unit, run of symbols) from a counter.  The counter and the TX carry buffers
+// are per-launch stream-ordered scratch, so concurrent launches never share.
+cudaError_t launch_one(KernelFn k, size_t smem, KParams& kp, bool tx, int N, cudaStream_t st) {
     if (!k) return cudaErrorInvalidValue;
     cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(k),
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    void* args[] = {const_cast<KParams*>(&kp)};
-    return cudaLaunchKernel(reinterpret_cast<const void*>(k), dim3(grid), dim3(kThreads), args, smem, st);
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(k), kThreads, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    const int grid = std::max(1, std::min(kp.n_items, per_sm * sms));
+    const size_t carry_bytes = tx ? (size_t)grid * (N / 2) * sizeof(float2) : 0;
+    void* scratch = nullptr;
+    e = cudaMallocAsync(&scratch, 256 + carry_bytes, st);
+    if (e != cudaSuccess) return e;
+    kp.item_counter = static_cast<int*>(scratch);
+    kp.carry = tx ? reinterpret_cast<float2*>(static_cast<char*>(scratch) + 256) : nullptr;
+    e = cudaMemsetAsync(scratch, 0, sizeof(int), st);
+    if (e == cudaSuccess) {
+        void* args[] = {&kp};
+        e = cudaLaunchKernel(reinterpret_cast<const void*>(k), dim3(grid), dim3(kThreads), args, smem, st);
+    }
+    const cudaError_t f = cudaFreeAsync(scratch, st);
+    return e != cudaSuccess ? e : f;
 }
 
 }  // namespace
@@ -98,6 +122,8 @@ void fill_common(const Plan& p, KParams& kp) {
     kp.zero_list = p.d_zero;
     kp.tw = p.d_tw;
     kp.stab_len = stab_len(p);
+    const char* dbg = std::getenv("FCW_DEBUG_SKIP");
+    kp.dbg_skip = dbg ? std::atoi(dbg) : 0;
 }
 
 size_t tx_smem_bytes(const Plan& p) { return smem_bytes(p, true, false); }
@@ -105,15 +131,17 @@ size_t rx_smem_bytes(const Plan& p) { return smem_bytes(p, false, true); }
 
 cudaError_t launch_tx(const Plan& p, KParams& kp, int S, cudaStream_t st) {
     const int LU = uniform_L(p);
-    kp.scratch_stride = scratch_stride(p, LU, false);
-    return launch_one(pick(p.N, LU).tx, smem_bytes(p, true, false), S * kp.nchunks, kp, st);
+    kp.scratch_stride = scratch_stride(p, LU, true, false);
+    kp.n_items = S * kp.nchunks;
+    return launch_one(pick(p.N, LU).tx, smem_bytes(p, true, false), kp, true, p.N, st);
 }
 
 cudaError_t launch_rx(const Plan& p, KParams& kp, int S, cudaStream_t st) {
     const int LU = uniform_L(p);
     const bool direct = !kp.fused;
-    kp.scratch_stride = scratch_stride(p, LU, direct);
-    return launch_one(pick(p.N, LU).rx, smem_bytes(p, false, direct), S * kp.nchunks, kp, st);
+    kp.scratch_stride = scratch_stride(p, LU, false, direct);
+    kp.n_items = S * kp.nchunks;
+    return launch_one(pick(p.N, LU).rx, smem_bytes(p, false, direct), kp, false, p.N, st);
 }
 
 // K-GEN: one thread per QAM symbol; splitmix64 is counter-based, so draw j of
