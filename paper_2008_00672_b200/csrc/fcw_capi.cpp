@@ -85,7 +85,15 @@ int pick_chunk(const fcw::Plan& p, int S, bool tx) {
     const long long resident = 2LL * 148;
     const long long per_cta = tx ? 16 : 32;
     long long c = ((long long)p.B * std::max(S, 1) + per_cta * resident - 1) / (per_cta * resident);
-    c = std::max<long long>(c, tx ? std::min(p.B, 8) : 1);
+    if (tx) {
+        // runs of >= 8 amortise the recomputed symbol, unless that would leave
+        // resident CTAs without work (few units): then fill the GPU first
+        long long floor_c = std::min(p.B, 8);
+        const long long fill = ((long long)p.B * std::max(S, 1) + resident - 1) / resident;
+        if ((long long)std::max(S, 1) * ((p.B + floor_c - 1) / floor_c) < resident)
+            floor_c = std::max<long long>(2, std::min(floor_c, fill));
+        c = std::max(c, floor_c);
+    }
     c = std::min<long long>(c, p.B);
     const long long nch = (p.B + c - 1) / c;  // rebalance run lengths
     return (int)((p.B + nch - 1) / nch);
