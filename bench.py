@@ -40,7 +40,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c5", choices=["c1", "c2", "c4", "c5"])
+    ap.add_argument("--config", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--rx", default="fused", choices=["fused", "direct"])
     ap.add_argument("--units", type=int, default=0, help="override total units (default: the config's)")
@@ -129,40 +129,52 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU legs
+def _banks(w):
+    """(Workload, offset) pairs: one for a plain workload, several for a mixed one."""
+    return list(zip(w.banks, w.offsets)) if hasattr(w, "banks") else [(w, 0)]
+
+
+def frame_samples(w) -> int:
+    return max(sum(b.N + c for c in b.cp) for b, _ in _banks(w))
+
+
 def cpu_reference(w, units: int, threads: int, fused: bool, steps: int = 1):
     """The reference's own path (oracle/_ref = unmodified fcwave + FFTW shim) on
-    `threads` host threads over `units` whole stream-frames.  Returns
+    `threads` host threads over `units` whole units.  A mixed workload runs
+    each numerology's bank through the reference separately (the reference
+    cannot express the mix; the offset sum is negligible).  Returns
     (Msamples/s per step list, kind, sample description)."""
     import oracle as O
 
-    plan_rows = sum(len(b) for b in w.active_maps)
-    packed = O.gen_grid(SEED, 0, units, w.B, plan_rows, w.bits_per_symbol).astype(np.complex64)
     vals = []
-    if O.ref_available():
-        kind = "reference"
-        for _ in range(steps):
-            t, _chk = O.Ref.bench_txrx(w.N, w.cp, [s.L for s in w.subbands], [s.c for s in w.subbands],
-                                       [s.window for s in w.subbands], [len(b) for b in w.active_maps],
-                                       w.active_maps, packed, units, threads, simplified=fused)
-            vals.append(units * sum(w.N + c for c in w.cp) / t / 1e6)
-    else:
-        kind = "port"
-        from concurrent.futures import ThreadPoolExecutor
+    kind = "reference" if O.ref_available() else "port"
+    packs = [O.gen_grid(SEED + i, 0, units, b.B, sum(len(x) for x in b.active_maps),
+                        w.bits_per_symbol).astype(np.complex64) for i, (b, _) in enumerate(_banks(w))]
+    for _ in range(steps):
+        t = 0.0
+        for (b, _), packed in zip(_banks(w), packs):
+            if kind == "reference":
+                dt, _chk = O.Ref.bench_txrx(b.N, b.cp, [s.L for s in b.subbands], [s.c for s in b.subbands],
+                                            [s.window for s in b.subbands], [len(x) for x in b.active_maps],
+                                            b.active_maps, packed, units, threads, simplified=fused)
+            else:
+                from concurrent.futures import ThreadPoolExecutor
 
-        sys.path.insert(0, os.path.join(ROOT, "tests"))
-        from helpers import oracle_rx, oracle_tx
+                sys.path.insert(0, os.path.join(ROOT, "tests"))
+                from helpers import oracle_rx, oracle_tx
 
-        def one(u):
-            wv, u0 = oracle_tx(w, packed[u].astype(np.complex128))
-            oracle_rx(w, wv, u0, fused)
+                def one(u, b=b, packed=packed):
+                    wv, u0 = oracle_tx(b, packed[u].astype(np.complex128))
+                    oracle_rx(b, wv, u0, fused)
 
-        for _ in range(steps):
-            t0 = time.perf_counter()
-            with ThreadPoolExecutor(threads) as ex:
-                list(ex.map(one, range(units)))
-            vals.append(units * sum(w.N + c for c in w.cp) / (time.perf_counter() - t0) / 1e6)
-    sample = (f"{units} whole {w.name} units (B={w.B} symbols, {len(w.subbands)} subbands each): "
-              f"tx_discontinuous over all subbands + rx_discontinuous per subband "
+                t0 = time.perf_counter()
+                with ThreadPoolExecutor(threads) as ex:
+                    list(ex.map(one, range(units)))
+                dt = time.perf_counter() - t0
+            t += dt
+        vals.append(units * frame_samples(w) / t / 1e6)
+    sample = (f"{units} whole {w.name} units ({', '.join(f'B={b.B}, {len(b.subbands)} subbands' for b, _ in _banks(w))}"
+              f"): tx_discontinuous over all subbands + rx_discontinuous per subband "
               f"({'fused' if fused else 'direct'}), one unit per thread; FFT via builder-written FFTW-API shim "
               f"(FFTW3 absent; an FFTW-backed reference would be faster)")
     return vals, kind, sample
@@ -198,6 +210,90 @@ def run_reference_arm(args, w):
 
 
 # ------------------------------------------------------------------ GPU arm
+class Runner:
+    """Device-resident TX+RX over S local units of a (plain or mixed) workload."""
+
+    def __init__(self, w, S: int, u0: int, dev, fused: bool):
+        import torch
+
+        self.w, self.S, self.fused = w, S, fused
+        self.mixed = hasattr(w, "banks")
+        self.plans = w.plans() if self.mixed else [w.plan()]
+        self.mx = w.mixed(self.plans) if self.mixed else None
+        self.Q = self.mx.Q if self.mixed else self.plans[0].Q
+        banks = w.banks if self.mixed else [w]
+        self.grids = []
+        for i, (b, p) in enumerate(zip(banks, self.plans)):
+            g = torch.empty((S, b.B, p.row_active), dtype=torch.complex64, device=dev)
+            p.gen_qam(SEED + i, u0, S, w.bits_per_symbol, g)
+            self.grids.append(g)
+        self.wave = torch.empty((S, self.Q), dtype=torch.complex64, device=dev)
+        self.outs = [torch.empty_like(g) for g in self.grids]
+        self.banks = banks
+
+    def tx(self, stream):
+        if self.mixed:
+            self.mx.tx(self.grids, self.wave, self.S, stream=stream)
+        else:
+            self.plans[0].tx(self.grids[0], self.wave, self.S, stream=stream)
+
+    def rx(self, stream):
+        if self.mixed:
+            self.mx.rx(self.wave, self.outs, self.S, fused=self.fused, stream=stream)
+        else:
+            p = self.plans[0]
+            p.rx(self.wave, p.Q, p.useful0, self.outs[0], self.S, fused=self.fused, stream=stream)
+
+    def algorithmic_bytes_per_unit(self) -> dict:
+        grid = sum(8 * b.B * p.row_active for b, p in zip(self.banks, self.plans))
+        wave = 8 * self.Q
+        return {"tx": grid + wave, "rx": grid + wave, "total": 2 * (grid + wave)}
+
+    def e2e(self, n_steps: int, dist, dev) -> float:
+        """Seconds per step through the host-buffer public API: grids H2D, TX,
+        waveform D2H; waveform H2D, RX, grids D2H (pinned host memory)."""
+        import torch
+
+        from paper_2008_00672_b200 import PinnedBuffer
+
+        if self.mixed:
+            # no host-buffer entry point composes banks: pinned torch copies around the device API
+            hg = [g.cpu().pin_memory() for g in self.grids]
+            hw = torch.empty(self.wave.shape, dtype=self.wave.dtype).pin_memory()
+            ho = [torch.empty(o.shape, dtype=o.dtype).pin_memory() for o in self.outs]
+
+            def one():
+                for d, h in zip(self.grids, hg):
+                    d.copy_(h, non_blocking=True)
+                self.tx(None)
+                hw.copy_(self.wave, non_blocking=True)
+                self.wave.copy_(hw, non_blocking=True)
+                self.rx(None)
+                for h, d in zip(ho, self.outs):
+                    h.copy_(d, non_blocking=True)
+                torch.cuda.synchronize()
+        else:
+            p = self.plans[0]
+            hg = PinnedBuffer((self.S, self.banks[0].B, p.row_active))
+            hw = PinnedBuffer((self.S, p.Q))
+            ho = PinnedBuffer((self.S, self.banks[0].B, p.row_active))
+            hg.array[...] = self.grids[0].cpu().numpy()
+            self.grids = self.outs = None
+            self.wave = None
+            torch.cuda.empty_cache()
+
+            def one():
+                p.tx_host(hg.array, self.S, out=hw.array)
+                p.rx_host(hw.array, p.Q, p.useful0, self.S, fused=self.fused, out=ho.array)
+        one()  # warm: staging buffers, streams
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(n_steps):
+            one()
+        return (time.perf_counter() - t0) / n_steps
+
+
 def main():
     args = parse()
     from paper_2008_00672_b200 import configs
@@ -218,23 +314,19 @@ def main():
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    plan = w.plan()
     u0, S = shard(w.units, rank, world)
-    fused = args.rx == "fused"
     dev = torch.device("cuda", local)
-    grid = torch.empty((S, w.B, plan.row_active), dtype=torch.complex64, device=dev)
-    wave = torch.empty((S, plan.Q), dtype=torch.complex64, device=dev)
-    out = torch.empty_like(grid)
-    plan.gen_qam(SEED, u0, S, w.bits_per_symbol, grid)
+    fused = args.rx == "fused"
+    run = Runner(w, S, u0, dev, fused)
     stream = torch.cuda.current_stream()
 
     def step(ev=None):
         if ev:
             ev[0].record(stream)
-        plan.tx(grid, wave, S, stream=stream)
+        run.tx(stream)
         if ev:
             ev[1].record(stream)
-        plan.rx(wave, plan.Q, plan.useful0, out, S, fused=fused, stream=stream)
+        run.rx(stream)
         if ev:
             ev[2].record(stream)
 
@@ -268,11 +360,11 @@ def main():
         dist.all_reduce(stats, op=dist.ReduceOp.MAX)
     elapsed_ms, tx_avg, rx_avg = [float(x) for x in stats.tolist()]
     ms_per_step = elapsed_ms / args.steps
-    total_samples = w.units * plan.frame_samples
+    total_samples = w.units * frame_samples(w)
     value = total_samples / (ms_per_step * 1e-3) / 1e6
 
     # roofline of the dominant kernel (algorithmic bytes per launch / mean launch time)
-    ab = configs.algorithmic_bytes_per_unit(w, plan.row_active, plan.Q)
+    ab = run.algorithmic_bytes_per_unit()
     peak, peak_src = hbm_peak()
     dom = "rx" if rx_avg > tx_avg else "tx"
     dom_ms = max(rx_avg, tx_avg)
@@ -282,46 +374,27 @@ def main():
     if os.path.exists(prof):
         try:
             with open(prof) as f:
-                tj = json.load(f)
-            t_ent = tj.get(w.name, {}).get(dom)
+                t_ent = json.load(f).get(w.name, {}).get(dom)
             if t_ent:
                 traffic = t_ent.get("dram_bytes_per_unit", 0) * S
         except Exception:
             traffic = None
     both_gbs = ab["total"] * S / (ms_per_step * 1e-3) / 1e9
+    launches_per_step = 2 * len(run.plans)
 
-    # e2e through the host-buffer C ABI (pinned host memory, copies in the timed region)
     e2e = None
     if not args.no_e2e:
-        from paper_2008_00672_b200 import PinnedBuffer
-
-        del out
-        torch.cuda.empty_cache()
-        hg = PinnedBuffer((S, w.B, plan.row_active))
-        hw = PinnedBuffer((S, plan.Q))
-        ho = PinnedBuffer((S, w.B, plan.row_active))
-        hg.array[...] = grid.cpu().numpy()
-        del grid, wave
-        torch.cuda.empty_cache()
-        plan.tx_host(hg.array, S, out=hw.array)  # warm (staging buffers, streams)
-        plan.rx_host(hw.array, plan.Q, plan.useful0, S, fused=fused, out=ho.array)
-        n_e2e = max(1, args.e2e_steps)
-        if dist:
-            dist.barrier()
-        t0 = time.perf_counter()
-        for _ in range(n_e2e):
-            plan.tx_host(hg.array, S, out=hw.array)
-            plan.rx_host(hw.array, plan.Q, plan.useful0, S, fused=fused, out=ho.array)
-        e2e_s = time.perf_counter() - t0
+        e2e_s = run.e2e(max(1, args.e2e_steps), dist, dev)
         t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
         if dist:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item()) / n_e2e
-        grid_b = 8 * w.B * plan.row_active * w.units
-        wave_b = 8 * plan.Q * w.units
+        e2e_s = float(t.item())
+        grid_b = (ab["tx"] - 8 * run.Q) * w.units
+        wave_b = 8 * run.Q * w.units
         e2e = {"value": total_samples / e2e_s / 1e6, "unit": UNIT, "h2d_bytes_per_step": grid_b + wave_b,
-               "d2h_bytes_per_step": wave_b + grid_b, "steps": n_e2e,
-               "path": "fcw_tx_host + fcw_rx_host (pinned host buffers, 2-stream H2D/kernel/D2H pipeline)"}
+               "d2h_bytes_per_step": wave_b + grid_b, "steps": max(1, args.e2e_steps),
+               "path": ("fcw_tx_host + fcw_rx_host (pinned host buffers, 2-stream H2D/kernel/D2H pipeline)"
+                        if not run.mixed else "pinned H2D + MixedNumerology.tx/rx + D2H")}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -331,20 +404,23 @@ def main():
         cpu = {"value": vals[0], "unit": UNIT, "cores": threads, "kind": kind, "sample": sample}
 
     if rank == 0:
+        N = max(b.N for b in run.banks)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": w.name, "units": w.units, "units_per_gpu": S, "symbols_per_unit": w.B,
-                       "subbands": len(w.subbands), "N": w.N, "rx_path": args.rx,
-                       "l2": "inputs larger than L2 (working set %.1f GB)" % (ab["total"] * w.units / 2 / 1e9),
+            "config": {"workload": w.name, "units": w.units, "units_per_gpu": S,
+                       "symbols_per_unit": [b.B for b in run.banks], "subbands": [len(b.subbands) for b in run.banks],
+                       "N": [b.N for b in run.banks], "rx_path": args.rx,
+                       "l2": "inputs larger than L2 (working set %.1f GB)" % (ab["total"] * w.units / 2 / 1e9)
+                       if ab["total"] * w.units / 2 > 126e6 else "working set fits L2 (small config)",
                        "description": w.description},
-            "roofline": {"bound": "hbm", "kernel": f"{dom}_kernel<{w.N}>", "achieved": achieved, "peak": peak,
+            "roofline": {"bound": "hbm", "kernel": f"{dom}_kernel<{N}>", "achieved": achieved, "peak": peak,
                          "unit": "GB/s", "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "algorithmic_bytes_per_unit": ab[dom],
                          "txrx_achieved_gbs": both_gbs, "txrx_frac": both_gbs / peak},
             "kernels_ms": {"tx": tx_avg, "rx": rx_avg},
-            "gpu_launches": 2 * args.steps,
+            "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks,
             "e2e": e2e,
             "cpu_baseline": cpu,

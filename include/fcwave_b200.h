@@ -43,6 +43,9 @@ extern "C" {
 #define FCW_RX_FUSED 2u  /* RX by transform decomposition (rx_symbol_simplified,
                             fc_sync.cpp:195-243); default is the direct path
                             (rx_symbol_direct, fc_sync.cpp:158-176) */
+#define FCW_TX_ACCUMULATE 4u /* TX adds into the waveform instead of storing it: the
+                            reference's subband sum w += sub (fc_sync.cpp:139),
+                            e.g. a second numerology's bank at a sample offset */
 
 /* Geometry of one FC bank (FcParams, numerology.hpp:34-41). */
 typedef struct fcw_fc_params {
@@ -111,7 +114,8 @@ int fcw_plan_fc_params(const fcw_plan* plan, int m, fcw_fc_params* out);
  *         or row_full (FCW_GRID_FULL); grid_unit_stride in complex elements
  *         (0 = B*row).
  *   wave: device complex64 [S][wave_unit_stride] (0 = Q); samples [0, Q) of
- *         each unit are written, useful0 = N_L.
+ *         each unit are written (or added to, with FCW_TX_ACCUMULATE),
+ *         useful0 = N_L.
  * Asynchronous on `stream` (cudaStream_t; NULL = legacy default stream). */
 int fcw_tx(const fcw_plan* plan, const void* grid, int64_t grid_unit_stride, void* wave,
            int64_t wave_unit_stride, int S, unsigned flags, void* stream);

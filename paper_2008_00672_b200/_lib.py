@@ -15,6 +15,7 @@ LIB_PATH = os.path.join(HERE, "lib", "libfcwave_b200.so")
 FCW_OK, FCW_EINVAL, FCW_ERANGE, FCW_ECUDA, FCW_ENOMEM, FCW_ENOTSUP = range(6)
 FCW_GRID_FULL = 1
 FCW_RX_FUSED = 2
+FCW_TX_ACCUMULATE = 4
 
 # Every symbol include/fcwave_b200.h declares (checked by tests/test_capi.py).
 EXPORTS = [

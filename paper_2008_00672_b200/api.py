@@ -16,7 +16,7 @@ from typing import Sequence
 import numpy as np
 
 from . import _lib
-from ._lib import FCW_GRID_FULL, FCW_RX_FUSED, check, lib
+from ._lib import FCW_GRID_FULL, FCW_RX_FUSED, FCW_TX_ACCUMULATE, check, lib
 
 
 # ------------------------------------------------------------------ geometry
@@ -277,9 +277,10 @@ class Plan:
 
     # -- device entry points
     def tx(self, grid, wave, S: int, full: bool = False, stream=None, grid_stride: int = 0,
-           wave_stride: int = 0) -> None:
-        check(lib().fcw_tx(self._h, _dev_ptr(grid), grid_stride, _dev_ptr(wave), wave_stride, S,
-                           FCW_GRID_FULL if full else 0, _stream_ptr(stream)))
+           wave_stride: int = 0, accumulate: bool = False) -> None:
+        flags = (FCW_GRID_FULL if full else 0) | (FCW_TX_ACCUMULATE if accumulate else 0)
+        check(lib().fcw_tx(self._h, _dev_ptr(grid), grid_stride, _dev_ptr(wave), wave_stride, S, flags,
+                           _stream_ptr(stream)))
 
     def rx(self, wave, wave_len: int, useful0: int, grid, S: int, fused: bool = True, full: bool = False,
            stream=None, wave_stride: int = 0, grid_stride: int = 0) -> None:
@@ -300,6 +301,9 @@ class Plan:
         check(lib().fcw_tx_host(self._h, g.ctypes.data, out.ctypes.data, S, FCW_GRID_FULL if full else 0))
         return out
 
+    def _raw(self):
+        return self._h
+
     def rx_host(self, wave: np.ndarray, wave_len: int, useful0: int, S: int, fused: bool = True, full: bool = False,
                 out: np.ndarray | None = None) -> np.ndarray:
         w = np.ascontiguousarray(wave, dtype=np.complex64)
@@ -310,6 +314,43 @@ class Plan:
         flags = (FCW_RX_FUSED if fused else 0) | (FCW_GRID_FULL if full else 0)
         check(lib().fcw_rx_host(self._h, w.ctypes.data, wave_len, useful0, out.ctypes.data, S, flags))
         return out
+
+
+class MixedNumerology:
+    """Several single-numerology FC banks sharing one sample rate and one
+    waveform (the paper's mixed-numerology use, Eq. (20b) with
+    N_OFDM,m per bank).  The reference can only express one numerology per
+    call (fc_sync.cpp:62-63,87); this composes banks on the device:
+
+      TX: bank 0 stores its waveform, every further bank ADDS its own at a
+          sample offset (FCW_TX_ACCUMULATE, the reference's `w += sub`,
+          fc_sync.cpp:139).
+      RX: each bank analyses the shared waveform with its own useful0
+          (offset + its N_L).
+
+    banks: list of (Plan, sample offset) with offsets >= 0.
+    """
+
+    def __init__(self, banks: Sequence[tuple[Plan, int]]):
+        if not banks:
+            raise ValueError("at least one bank required")
+        self.banks = [(p, int(off)) for p, off in banks]
+        for _, off in self.banks:
+            if off < 0:
+                raise ValueError("bank offsets must be >= 0")
+        self.Q = max(off + p.Q for p, off in self.banks)
+        self.frame_samples = max(p.frame_samples for p, _ in self.banks)
+
+    def tx(self, grids, wave, S: int, stream=None) -> None:
+        """grids[i]: device packed grid of bank i; wave: device complex64 [S][Q]."""
+        base = _dev_ptr(wave)
+        for i, ((p, off), g) in enumerate(zip(self.banks, grids)):
+            p.tx(g, base + 8 * off, S, stream=stream, wave_stride=self.Q, accumulate=i > 0)
+
+    def rx(self, wave, outs, S: int, fused: bool = True, stream=None) -> None:
+        base = _dev_ptr(wave)
+        for (p, off), o in zip(self.banks, outs):
+            p.rx(base, self.Q, off + p.useful0, o, S, fused=fused, stream=stream, wave_stride=self.Q)
 
 
 class PinnedBuffer:

@@ -92,7 +92,53 @@ def config5(streams: int = 64, frames: int = 8) -> Workload:
                     "64 antenna streams x 8 frames")
 
 
-CONFIGS = {"c1": config1, "c2": config2, "c4": config4, "c5": config5}
+@dataclass
+class MixedWorkload:
+    """Config 3: two numerologies on one 30.72 Msps carrier.
+    Bank A: 15 kHz, N=2048, 48 PRB (576 sc), L=1024, CP 144, 14 symbols.
+    Bank B: 30 kHz, N=1024, 24 PRB (288 sc), L=512, CP 72, 28 symbols.
+    Guard: 2 PRB at 30 kHz (720 kHz) between them.  Both span 1 ms; B's
+    waveform is offset by +184 samples so both symbol-0 CPs start together."""
+
+    name: str
+    banks: list[Workload]
+    offsets: list[int]
+    bits_per_symbol: int
+    units: int
+    description: str
+
+    def plans(self) -> list[api.Plan]:
+        return [w.plan() for w in self.banks]
+
+    def mixed(self, plans: list[api.Plan]) -> api.MixedNumerology:
+        return api.MixedNumerology(list(zip(plans, self.offsets)))
+
+
+def config3() -> MixedWorkload:
+    fs_khz = 30720
+    # bank A (15 kHz bins on N=2048): occupies [-9.00, -0.36) MHz
+    NA, NB = 2048, 1024
+    a_lo = -600  # in 15 kHz bins
+    a_sc = 576
+    cA = (a_lo + a_sc // 2) % NA
+    subA = api.SubbandConfig(L=1024, c=cA, window=api.design_window(1024, a_sc, 4), n_active=a_sc, n_tb=4)
+    wA = Workload("c3_bankA_15khz", NA, 15, [144] * 14, [subA], [api.centered_active_map(1024, a_sc, False)], 6, 1,
+                  "15 kHz, N=2048, 48 PRB, L=1024")
+    # bank B (30 kHz bins on N=1024): occupies [+0.36, +9.00) MHz
+    b_lo = 12  # in 30 kHz bins (guard [-0.36, +0.36) MHz = 2 PRB at 30 kHz)
+    b_sc = 288
+    cB = (b_lo + b_sc // 2) % NB
+    subB = api.SubbandConfig(L=512, c=cB, window=api.design_window(512, b_sc, 4), n_active=b_sc, n_tb=4)
+    wB = Workload("c3_bankB_30khz", NB, 30, [72] * 28, [subB], [api.centered_active_map(512, b_sc, False)], 6, 1,
+                  "30 kHz, N=1024, 24 PRB, L=512")
+    # align the symbol-0 CP starts: N_L,A - N_CP,A = 512 - 144 = 368; N_L,B - N_CP,B = 256 - 72 = 184
+    off_b = (NA // 4 - 144) - (NB // 4 - 72)
+    assert fs_khz == 15 * NA == 30 * NB
+    return MixedWorkload("c3_mixed_numerology_20mhz", [wA, wB], [0, off_b], 6, 1024,
+                         "15 kHz N=2048 48 PRB + 30 kHz N=1024 24 PRB, 2 PRB guard, 64-QAM, 1 ms units, fused RX")
+
+
+CONFIGS = {"c1": config1, "c2": config2, "c3": config3, "c4": config4, "c5": config5}
 
 
 def get(name: str, **kw) -> Workload:

@@ -582,6 +582,7 @@ int fcw_tx(const fcw_plan* p, const void* grid, int64_t grid_stride, void* wave,
     kp.nchunks = (p->B + kp.chunk - 1) / kp.chunk;
     kp.row_len = row;
     kp.grid_full = (flags & FCW_GRID_FULL) ? 1 : 0;
+    kp.accumulate = (flags & FCW_TX_ACCUMULATE) ? 1 : 0;
     kp.in = static_cast<const float2*>(grid);
     kp.in_stride = grid_stride;
     kp.out = static_cast<float2*>(wave);

@@ -550,7 +550,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) tx_kernel(const KP
                     if (mm >= 8) val = cadd(val, v[1][mm - 8]);
                     if (mm < 8) val = cadd(val, cr[mm]);
                     if (u < sy.own_len) {
-                        if (emit) dst[u] = val;
+                        if (emit) dst[u] = P.accumulate ? cadd(dst[u], val) : val;
                     } else {
                         carry[u - sy.own_len] = val;
                     }

@@ -56,6 +56,7 @@ struct KParams {
     int row_len;
     int grid_full;
     int fused;
+    int accumulate;      // TX: add into the waveform instead of storing (FCW_TX_ACCUMULATE)
     int dbg_skip;        // dev-only timing knob (FCW_DEBUG_SKIP): 1 = short stage, 2 = long transform
     int n_ext, n_zero, n_lvl;
     int lvl_start[kMaxLevels + 1];

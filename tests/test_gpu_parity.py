@@ -194,3 +194,49 @@ def test_chunk_boundaries_full_frame(chunk, monkeypatch):
 
 
 _FULL: dict = {}
+
+
+# ------------------------------------------------------- config 3 (mixed)
+def test_c3_mixed_numerology():
+    """Two numerologies summed on one waveform: glue = two oracle calls + an
+    offset sum (parity unpinned by the reference, which cannot express it)."""
+    mw = configs.config3()
+    plans = mw.plans()
+    mixed = mw.mixed(plans)
+    S = 2
+    grids = []
+    for i, (w, p) in enumerate(zip(mw.banks, plans)):
+        g = torch.empty((S, w.B, p.row_active), dtype=torch.complex64, device="cuda")
+        p.gen_qam(SEED + i, 0, S, mw.bits_per_symbol, g)
+        grids.append(g)
+    wave = torch.empty((S, mixed.Q), dtype=torch.complex64, device="cuda")
+    mixed.tx(grids, wave, S)
+    torch.cuda.synchronize()
+    assert mixed.Q == 31568 and mw.offsets == [0, 184]
+    for u in range(S):
+        want = np.zeros(mixed.Q, np.complex128)
+        for (w, p), off, g in zip(zip(mw.banks, plans), mw.offsets, grids):
+            wv, u0 = oracle_tx(w, g[u].cpu().numpy().astype(np.complex128))
+            want[off:off + len(wv)] += wv
+        assert rel_rms(wave[u].cpu().numpy(), want) <= TOL
+        outs = [torch.empty((S, w.B, p.row_active), dtype=torch.complex64, device="cuda")
+                for w, p in zip(mw.banks, plans)]
+        mixed.rx(_dev(np.stack([want] * S)), outs, S, fused=True)
+        torch.cuda.synchronize()
+        for (w, p), off, o in zip(zip(mw.banks, plans), mw.offsets, outs):
+            rp, _ = oracle_rx(w, want, off + p.useful0, True)
+            assert rel_rms(o[u].cpu().numpy(), rp) <= TOL
+
+
+def test_tx_accumulate_adds():
+    w = truncate(configs.config5(), 16)
+    plan = w.plan()
+    S = 2
+    grid = torch.empty((S, w.B, plan.row_active), dtype=torch.complex64, device="cuda")
+    plan.gen_qam(SEED, 0, S, w.bits_per_symbol, grid)
+    a = torch.empty((S, plan.Q), dtype=torch.complex64, device="cuda")
+    plan.tx(grid, a, S)
+    b = a.clone()
+    plan.tx(grid, b, S, accumulate=True)
+    torch.cuda.synchronize()
+    assert torch.allclose(b, 2 * a, rtol=1e-6, atol=1e-7)
