@@ -82,7 +82,7 @@ int pick_chunk(const fcw::Plan& p, int S, bool tx) {
         const int c = std::atoi(e);
         if (c > 0) return std::min(c, p.B);
     }
-    const long long resident = 2LL * 148;
+    const long long resident = 2LL * 148 * ((p.N >= 512 && p.N <= 4096) ? 4096 / p.N : 1);  // teams
     const long long per_cta = tx ? 16 : 32;
     long long c = ((long long)p.B * std::max(S, 1) + per_cta * resident - 1) / (per_cta * resident);
     if (tx) {

@@ -107,13 +107,20 @@ FCW_DI float2 grid_val(const KParams& P, const SubDev& sd, const float2* __restr
     return inv >= 0 ? row[sd.act_off + inv] : zero2();
 }
 
+// The threads that share one symbol's spectra: the whole CTA for N = 4096 (or
+// N < 512), else one of G = 4096/N independent sub-teams of N/16 threads.
+struct Team {
+    int tid, nthr;    // thread index / count within the team
+    int warp, nwarp;  // warp index / count within the team
+};
+
 // ---------------------------------------------------------------- K-TX parts
 
 // Short-side TX of one subband-symbol by one thread (L <= 32).
 template <int N, int L>
-FCW_DI void tx_short_thread(const KParams& P, const SymDev& sy, const float2* __restrict__ row,
+FCW_DI void tx_short_thread(const KParams& P, const Team& tm, const SymDev& sy, const float2* __restrict__ row,
                             float2* spec0, float2* spec1, int gstart, int gcount) {
-    for (int i = threadIdx.x; i < gcount; i += kThreads) {
+    for (int i = tm.tid; i < gcount; i += tm.nthr) {
         const int m = P.grp_sub ? __ldg(&P.grp_sub[gstart + i]) : gstart + i;
         const SubDev sd = P.sub[m];
         float2 x[L];
@@ -147,13 +154,13 @@ FCW_DI void tx_short_thread(const KParams& P, const SymDev& sy, const float2* __
 // Short-side TX of one subband-symbol by one warp (L >= 64), lane holds bins
 // lane + 32k.  One padded scratch buffer per warp.
 template <int N, int L>
-FCW_DI void tx_short_warp(const KParams& P, const SymDev& sy, const float2* __restrict__ row,
+FCW_DI void tx_short_warp(const KParams& P, const Team& tm, const SymDev& sy, const float2* __restrict__ row,
                           float2* spec0, float2* spec1, float2* scr, const float2* stw, int gstart, int gcount) {
     constexpr int PPT = L / 32;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
     const int sts = P.stab_len / L;
     float2* const b1[1] = {scr};
-    for (int i = warp; i < gcount; i += kWarps) {
+    for (int i = tm.warp; i < gcount; i += tm.nwarp) {
         const int m = P.grp_sub ? __ldg(&P.grp_sub[gstart + i]) : gstart + i;
         const SubDev sd = P.sub[m];
         const float2 ph = cscale(tw_conj(P.tw, theta_exp<N>(sd.cmodN, sy.smodN)), sd.tx_scale);
@@ -221,34 +228,34 @@ FCW_DI void tx_short_warp(const KParams& P, const SymDev& sy, const float2* __re
 }
 
 template <int N, int L>
-FCW_DI void tx_short_one(const KParams& P, const SymDev& sy, const float2* __restrict__ row, float2* spec0,
-                         float2* spec1, float2* scr, const float2* stw, int gs, int gc) {
+FCW_DI void tx_short_one(const KParams& P, const Team& tm, const SymDev& sy, const float2* __restrict__ row,
+                         float2* spec0, float2* spec1, float2* scr, const float2* stw, int gs, int gc) {
     if constexpr (L <= N) {
         if constexpr (L <= 32)
-            tx_short_thread<N, L>(P, sy, row, spec0, spec1, gs, gc);
+            tx_short_thread<N, L>(P, tm, sy, row, spec0, spec1, gs, gc);
         else
-            tx_short_warp<N, L>(P, sy, row, spec0, spec1, scr, stw, gs, gc);
+            tx_short_warp<N, L>(P, tm, sy, row, spec0, spec1, scr, stw, gs, gc);
     }
 }
 
 template <int N, int LU>
-FCW_DI void tx_short_all(const KParams& P, const SymDev& sy, const float2* __restrict__ row, float2* spec0,
-                         float2* spec1, float2* scr, const float2* stw) {
+FCW_DI void tx_short_all(const KParams& P, const Team& tm, const SymDev& sy, const float2* __restrict__ row,
+                         float2* spec0, float2* spec1, float2* scr, const float2* stw) {
     if constexpr (LU > 0) {
-        tx_short_one<N, LU>(P, sy, row, spec0, spec1, scr, stw, 0, P.M);
+        tx_short_one<N, LU>(P, tm, sy, row, spec0, spec1, scr, stw, 0, P.M);
     } else {
         for (int g = 0; g < P.n_groups; ++g) {
             const int gs = P.grp_start[g], gc = P.grp_count[g];
             switch (P.grp_L[g]) {
-                case 4: tx_short_one<N, 4>(P, sy, row, spec0, spec1, scr, stw, gs, gc); break;
-                case 8: tx_short_one<N, 8>(P, sy, row, spec0, spec1, scr, stw, gs, gc); break;
-                case 16: tx_short_one<N, 16>(P, sy, row, spec0, spec1, scr, stw, gs, gc); break;
-                case 32: tx_short_one<N, 32>(P, sy, row, spec0, spec1, scr, stw, gs, gc); break;
-                case 64: tx_short_one<N, 64>(P, sy, row, spec0, spec1, scr, stw, gs, gc); break;
-                case 128: tx_short_one<N, 128>(P, sy, row, spec0, spec1, scr, stw, gs, gc); break;
-                case 256: tx_short_one<N, 256>(P, sy, row, spec0, spec1, scr, stw, gs, gc); break;
-                case 512: tx_short_one<N, 512>(P, sy, row, spec0, spec1, scr, stw, gs, gc); break;
-                case 1024: tx_short_one<N, 1024>(P, sy, row, spec0, spec1, scr, stw, gs, gc); break;
+                case 4: tx_short_one<N, 4>(P, tm, sy, row, spec0, spec1, scr, stw, gs, gc); break;
+                case 8: tx_short_one<N, 8>(P, tm, sy, row, spec0, spec1, scr, stw, gs, gc); break;
+                case 16: tx_short_one<N, 16>(P, tm, sy, row, spec0, spec1, scr, stw, gs, gc); break;
+                case 32: tx_short_one<N, 32>(P, tm, sy, row, spec0, spec1, scr, stw, gs, gc); break;
+                case 64: tx_short_one<N, 64>(P, tm, sy, row, spec0, spec1, scr, stw, gs, gc); break;
+                case 128: tx_short_one<N, 128>(P, tm, sy, row, spec0, spec1, scr, stw, gs, gc); break;
+                case 256: tx_short_one<N, 256>(P, tm, sy, row, spec0, spec1, scr, stw, gs, gc); break;
+                case 512: tx_short_one<N, 512>(P, tm, sy, row, spec0, spec1, scr, stw, gs, gc); break;
+                case 1024: tx_short_one<N, 1024>(P, tm, sy, row, spec0, spec1, scr, stw, gs, gc); break;
                 default: break;
             }
         }
@@ -258,9 +265,9 @@ FCW_DI void tx_short_all(const KParams& P, const SymDev& sy, const float2* __res
 // ---------------------------------------------------------------- K-RX parts
 
 template <int N, int L>
-FCW_DI void rx_short_thread(const KParams& P, const SymDev& sy, const float2* spec0, const float2* spec1,
-                            float2* __restrict__ orow, int gstart, int gcount) {
-    for (int i = threadIdx.x; i < gcount; i += kThreads) {
+FCW_DI void rx_short_thread(const KParams& P, const Team& tm, const SymDev& sy, const float2* spec0,
+                            const float2* spec1, float2* __restrict__ orow, int gstart, int gcount) {
+    for (int i = tm.tid; i < gcount; i += tm.nthr) {
         const int m = P.grp_sub ? __ldg(&P.grp_sub[gstart + i]) : gstart + i;
         const SubDev sd = P.sub[m];
         // rx_block_freq (fc_sync.cpp:178-193) without the per-symbol rotator,
@@ -332,13 +339,14 @@ FCW_DI void rx_short_thread(const KParams& P, const SymDev& sy, const float2* sp
 }
 
 template <int N, int L>
-FCW_DI void rx_short_warp(const KParams& P, const SymDev& sy, const float2* spec0, const float2* spec1,
-                          float2* __restrict__ orow, float2* scr, const float2* stw, int gstart, int gcount) {
+FCW_DI void rx_short_warp(const KParams& P, const Team& tm, const SymDev& sy, const float2* spec0,
+                          const float2* spec1, float2* __restrict__ orow, float2* scr, const float2* stw, int gstart,
+                          int gcount) {
     constexpr int PPT = L / 32;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
     const int sts = P.stab_len / L;
     float2* const b1[1] = {scr};
-    for (int i = warp; i < gcount; i += kWarps) {
+    for (int i = tm.warp; i < gcount; i += tm.nwarp) {
         const int m = P.grp_sub ? __ldg(&P.grp_sub[gstart + i]) : gstart + i;
         const SubDev sd = P.sub[m];
         float2 g0[1][PPT], g1[1][PPT];
@@ -420,34 +428,34 @@ FCW_DI void rx_short_warp(const KParams& P, const SymDev& sy, const float2* spec
 }
 
 template <int N, int L>
-FCW_DI void rx_short_one(const KParams& P, const SymDev& sy, const float2* spec0, const float2* spec1,
-                         float2* orow, float2* scr, const float2* stw, int gs, int gc) {
+FCW_DI void rx_short_one(const KParams& P, const Team& tm, const SymDev& sy, const float2* spec0,
+                         const float2* spec1, float2* orow, float2* scr, const float2* stw, int gs, int gc) {
     if constexpr (L <= N) {
         if constexpr (L <= 32)
-            rx_short_thread<N, L>(P, sy, spec0, spec1, orow, gs, gc);
+            rx_short_thread<N, L>(P, tm, sy, spec0, spec1, orow, gs, gc);
         else
-            rx_short_warp<N, L>(P, sy, spec0, spec1, orow, scr, stw, gs, gc);
+            rx_short_warp<N, L>(P, tm, sy, spec0, spec1, orow, scr, stw, gs, gc);
     }
 }
 
 template <int N, int LU>
-FCW_DI void rx_short_all(const KParams& P, const SymDev& sy, const float2* spec0, const float2* spec1,
-                         float2* orow, float2* scr, const float2* stw) {
+FCW_DI void rx_short_all(const KParams& P, const Team& tm, const SymDev& sy, const float2* spec0,
+                         const float2* spec1, float2* orow, float2* scr, const float2* stw) {
     if constexpr (LU > 0) {
-        rx_short_one<N, LU>(P, sy, spec0, spec1, orow, scr, stw, 0, P.M);
+        rx_short_one<N, LU>(P, tm, sy, spec0, spec1, orow, scr, stw, 0, P.M);
     } else {
         for (int g = 0; g < P.n_groups; ++g) {
             const int gs = P.grp_start[g], gc = P.grp_count[g];
             switch (P.grp_L[g]) {
-                case 4: rx_short_one<N, 4>(P, sy, spec0, spec1, orow, scr, stw, gs, gc); break;
-                case 8: rx_short_one<N, 8>(P, sy, spec0, spec1, orow, scr, stw, gs, gc); break;
-                case 16: rx_short_one<N, 16>(P, sy, spec0, spec1, orow, scr, stw, gs, gc); break;
-                case 32: rx_short_one<N, 32>(P, sy, spec0, spec1, orow, scr, stw, gs, gc); break;
-                case 64: rx_short_one<N, 64>(P, sy, spec0, spec1, orow, scr, stw, gs, gc); break;
-                case 128: rx_short_one<N, 128>(P, sy, spec0, spec1, orow, scr, stw, gs, gc); break;
-                case 256: rx_short_one<N, 256>(P, sy, spec0, spec1, orow, scr, stw, gs, gc); break;
-                case 512: rx_short_one<N, 512>(P, sy, spec0, spec1, orow, scr, stw, gs, gc); break;
-                case 1024: rx_short_one<N, 1024>(P, sy, spec0, spec1, orow, scr, stw, gs, gc); break;
+                case 4: rx_short_one<N, 4>(P, tm, sy, spec0, spec1, orow, scr, stw, gs, gc); break;
+                case 8: rx_short_one<N, 8>(P, tm, sy, spec0, spec1, orow, scr, stw, gs, gc); break;
+                case 16: rx_short_one<N, 16>(P, tm, sy, spec0, spec1, orow, scr, stw, gs, gc); break;
+                case 32: rx_short_one<N, 32>(P, tm, sy, spec0, spec1, orow, scr, stw, gs, gc); break;
+                case 64: rx_short_one<N, 64>(P, tm, sy, spec0, spec1, orow, scr, stw, gs, gc); break;
+                case 128: rx_short_one<N, 128>(P, tm, sy, spec0, spec1, orow, scr, stw, gs, gc); break;
+                case 256: rx_short_one<N, 256>(P, tm, sy, spec0, spec1, orow, scr, stw, gs, gc); break;
+                case 512: rx_short_one<N, 512>(P, tm, sy, spec0, spec1, orow, scr, stw, gs, gc); break;
+                case 1024: rx_short_one<N, 1024>(P, tm, sy, spec0, spec1, orow, scr, stw, gs, gc); break;
                 default: break;
             }
         }
@@ -461,90 +469,131 @@ constexpr int min_blocks() {
     return (LU >= 64 || (LU > 0 && LU <= 16)) ? 2 : 1;
 }
 
-// Next work item (unit, run of symbols) for this persistent CTA: dynamic
-// scheduling through one global counter keeps the tail short.
-FCW_DI int next_item(const KParams& P, int* s_item) {
-    __syncthreads();  // everyone has read the previous item id
-    if (threadIdx.x == 0) *s_item = atomicAdd(P.item_counter, 1);
-    __syncthreads();
+// Sub-teams per CTA: the long transform of one block needs N/16 threads, so a
+// 256-thread CTA runs 4096/N independent teams for 512 <= N <= 4096 (each with
+// its own spectra, work items and named barrier); smaller N use one team.
+template <int N>
+constexpr int teams_per_cta() {
+    return (N >= 512 && N <= 4096) ? 4096 / N : 1;
+}
+
+// Team-scope barrier: the CTA barrier for a single team, else named barrier
+// 1 + g over the team's threads (bar.sync counts must be warp multiples).
+template <int G>
+FCW_DI void team_sync(int g, int nthr) {
+    if constexpr (G == 1)
+        __syncthreads();
+    else
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(nthr) : "memory");
+}
+
+// Next work item (unit, run of symbols) for this team: dynamic scheduling
+// through one global counter keeps the tail short.
+template <int G>
+FCW_DI int next_item(const KParams& P, int* s_item, int g, int gtid, int nthr) {
+    team_sync<G>(g, nthr);  // everyone has read the previous item id
+    if (gtid == 0) *s_item = atomicAdd(P.item_counter, 1);
+    team_sync<G>(g, nthr);
     return *s_item;
+}
+
+// Shared layout of both kernels' SMEM: G teams x {spec0, spec1}, then one
+// warp scratch per warp, the short twiddle table and G item slots.
+struct Smem {
+    float2 *spec0, *spec1, *scr, *stw;
+    int* s_item;
+};
+template <int G>
+FCW_DI Smem smem_layout(const KParams& P, int g) {
+    extern __shared__ float4 smem_raw[];
+    float2* sm = reinterpret_cast<float2*>(smem_raw);
+    Smem s;
+    s.spec0 = sm + (2 * g) * P.spec_stride;
+    s.spec1 = s.spec0 + P.spec_stride;
+    float2* rest = sm + 2 * G * P.spec_stride;
+    s.scr = rest + (threadIdx.x >> 5) * P.scratch_stride;
+    s.stw = rest + kWarps * P.scratch_stride;
+    s.s_item = reinterpret_cast<int*>(s.stw + P.stab_len) + g;
+    return s;
 }
 
 template <int N, int LU>
 __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) tx_kernel(const KParams P) {
-    extern __shared__ float4 smem_raw[];
-    float2* sm = reinterpret_cast<float2*>(smem_raw);
-    float2* spec0 = sm;
-    float2* spec1 = sm + P.spec_stride;
-    float2* scr = spec1 + P.spec_stride + (threadIdx.x >> 5) * P.scratch_stride;
-    float2* stw = spec1 + P.spec_stride + kWarps * P.scratch_stride;  // W_{stab_len} for the short transforms
-    int* s_item = reinterpret_cast<int*>(stw + P.stab_len);
-    // The block-1 tail that overlaps the next symbol lives in a per-CTA global
-    // (L2-resident) buffer: written and read back by this CTA only.
-    float2* carry = P.carry + (long long)blockIdx.x * (N / 2);
-    constexpr int T = N / kPPT;
+    constexpr int G = teams_per_cta<N>();
+    constexpr int T = N / kPPT;                  // long-transform threads per team
+    constexpr int TT = G == 1 ? kThreads : T;    // threads per team
     const int tid = threadIdx.x;
-    const bool act = tid < T;
-    for (int i = tid; i < P.stab_len; i += kThreads) stw[i] = __ldg(&P.tw[i * (N / P.stab_len)]);
+    const int g = tid / TT, gtid = tid - g * TT;
+    const bool act = gtid < T;
+    const Team tm{gtid, TT, gtid >> 5, TT / 32};
+    const Smem S = smem_layout<G>(P, g);
+    float2 *spec0 = S.spec0, *spec1 = S.spec1;
+    // The block-1 tail that overlaps the next symbol lives in a per-team global
+    // (L2-resident) buffer: written and read back by this team only.
+    float2* carry = P.carry + ((long long)blockIdx.x * G + g) * (N / 2);
+    for (int i = tid; i < P.stab_len; i += kThreads) S.stw[i] = __ldg(&P.tw[i * (N / P.stab_len)]);
+    __syncthreads();
 
-    for (int item = next_item(P, s_item); item < P.n_items; item = next_item(P, s_item)) {
+    for (int item = next_item<G>(P, S.s_item, g, gtid, TT); item < P.n_items;
+         item = next_item<G>(P, S.s_item, g, gtid, TT)) {
         const int unit = item / P.nchunks;
         const int n0 = (item % P.nchunks) * P.chunk;
         const int n1 = min(P.B, n0 + P.chunk);
         const float2* in_u = P.in + (long long)unit * P.in_stride;
         float2* out_u = P.out + (long long)unit * P.out_stride;
         const int nfirst = n0 > 0 ? n0 - 1 : 0;
-        if (tid == 0) prefetch_l2(in_u + (long long)nfirst * P.row_len, 8LL * P.row_len);
+        if (gtid == 0) prefetch_l2(in_u + (long long)nfirst * P.row_len, 8LL * P.row_len);
 
         for (int n = nfirst; n < n1; ++n) {
             const SymDev sy = P.sym[n];
-            __syncthreads();  // previous symbol's transform no longer reads spec
-            if (tid == 0 && n + 1 < n1) prefetch_l2(in_u + (long long)(n + 1) * P.row_len, 8LL * P.row_len);
+            team_sync<G>(g, TT);  // previous symbol's transform no longer reads spec
+            if (gtid == 0 && n + 1 < n1) prefetch_l2(in_u + (long long)(n + 1) * P.row_len, 8LL * P.row_len);
             if (!(P.dbg_skip & 1))
-                tx_short_all<N, LU>(P, sy, in_u + (long long)n * P.row_len, spec0, spec1, scr, stw);
-            __syncthreads();
+                tx_short_all<N, LU>(P, tm, sy, in_u + (long long)n * P.row_len, spec0, spec1, S.scr, S.stw);
+            team_sync<G>(g, TT);
             // secondary contributions of shared transition bins, in rank order
             for (int l = 0; l < P.n_lvl; ++l) {
-                for (int k = P.lvl_start[l] + tid; k < P.lvl_start[l + 1]; k += kThreads) {
+                for (int k = P.lvl_start[l] + gtid; k < P.lvl_start[l + 1]; k += TT) {
                     const int q = __ldg(&P.fix_tgt[k]), e = N + __ldg(&P.fix_slot[k]);
                     spec0[q] = cadd(spec0[q], spec0[e]);
                     spec1[q] = cadd(spec1[q], spec1[e]);
                 }
-                __syncthreads();
+                team_sync<G>(g, TT);
             }
-            for (int k = tid; k < P.n_zero; k += kThreads) {
+            for (int k = gtid; k < P.n_zero; k += TT) {
                 const int q = __ldg(&P.zero_list[k]);
                 spec0[q] = zero2();
                 spec1[q] = zero2();
             }
-            __syncthreads();
+            team_sync<G>(g, TT);
 
             float2 cr[8];
 #pragma unroll
             for (int m = 0; m < 8; ++m) {
-                const int u = tid + T * m;
+                const int u = gtid + T * m;
                 cr[m] = (act && n > nfirst && u < sy.carry_len) ? carry[u] : zero2();
             }
             float2 v[2][kPPT];
             if (act) {
 #pragma unroll
                 for (int m = 0; m < kPPT; ++m) {
-                    v[0][m] = spec0[tid + T * m];
-                    v[1][m] = spec1[tid + T * m];
+                    v[0][m] = spec0[gtid + T * m];
+                    v[1][m] = spec1[gtid + T * m];
                 }
             }
             {
                 float2* const bufs[2] = {spec0, spec1};
-                if (!(P.dbg_skip & 2)) team_fft<N, T, kPPT, +1, 2, true>(v, bufs, P.tw, 1, tid, act);
+                if (!(P.dbg_skip & 2))
+                    team_fft<N, T, kPPT, +1, 2, true>(v, bufs, P.tw, 1, gtid, act, G == 1 ? 0 : 1 + g, TT);
             }
-            __syncthreads();  // every thread has read its carry before it is overwritten
+            team_sync<G>(g, TT);  // every thread has read its carry before it is overwritten
             // symbol-wise overlap-add: block 0 at 0, block 1 at N/2, carry from n-1
             if (act) {
                 const bool emit = n >= n0;
                 float2* dst = out_u + sy.sigma;
 #pragma unroll
                 for (int mm = 0; mm < 24; ++mm) {
-                    const int u = tid + T * mm;
+                    const int u = gtid + T * mm;
                     float2 val = zero2();
                     if (mm < 16) val = v[0][mm];
                     if (mm >= 8) val = cadd(val, v[1][mm - 8]);
@@ -562,33 +611,34 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) tx_kernel(const KP
 
 template <int N, int LU>
 __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) rx_kernel(const KParams P) {
-    extern __shared__ float4 smem_raw[];
-    float2* sm = reinterpret_cast<float2*>(smem_raw);
-    float2* spec0 = sm;
-    float2* spec1 = sm + P.spec_stride;
-    float2* scr = spec1 + P.spec_stride + (threadIdx.x >> 5) * P.scratch_stride;
-    float2* stw = spec1 + P.spec_stride + kWarps * P.scratch_stride;
-    int* s_item = reinterpret_cast<int*>(stw + P.stab_len);
+    constexpr int G = teams_per_cta<N>();
     constexpr int T = N / kPPT;
+    constexpr int TT = G == 1 ? kThreads : T;
     const int tid = threadIdx.x;
-    const bool act = tid < T;
-    for (int i = tid; i < P.stab_len; i += kThreads) stw[i] = __ldg(&P.tw[i * (N / P.stab_len)]);
+    const int g = tid / TT, gtid = tid - g * TT;
+    const bool act = gtid < T;
+    const Team tm{gtid, TT, gtid >> 5, TT / 32};
+    const Smem S = smem_layout<G>(P, g);
+    float2 *spec0 = S.spec0, *spec1 = S.spec1;
+    for (int i = tid; i < P.stab_len; i += kThreads) S.stw[i] = __ldg(&P.tw[i * (N / P.stab_len)]);
+    __syncthreads();
 
-    for (int item = next_item(P, s_item); item < P.n_items; item = next_item(P, s_item)) {
+    for (int item = next_item<G>(P, S.s_item, g, gtid, TT); item < P.n_items;
+         item = next_item<G>(P, S.s_item, g, gtid, TT)) {
         const int unit = item / P.nchunks;
         const int n0 = (item % P.nchunks) * P.chunk;
         const int n1 = min(P.B, n0 + P.chunk);
         const float2* in_u = P.in + (long long)unit * P.in_stride;
         float2* out_u = P.out + (long long)unit * P.out_stride;
-        if (tid == 0) prefetch_l2(in_u + P.rx_base + P.sym[n0].sigma, 8LL * (3 * N / 2));
+        if (gtid == 0) prefetch_l2(in_u + P.rx_base + P.sym[n0].sigma, 8LL * (3 * N / 2));
 
         for (int n = n0; n < n1; ++n) {
             const SymDev sy = P.sym[n];
-            if (tid == 0 && n + 1 < n1) prefetch_l2(in_u + P.rx_base + P.sym[n + 1].sigma, 8LL * (3 * N / 2));
+            if (gtid == 0 && n + 1 < n1) prefetch_l2(in_u + P.rx_base + P.sym[n + 1].sigma, 8LL * (3 * N / 2));
             float2 v[2][kPPT];
             if (act) {
                 // rx_segment (fc_sync.cpp:145-156): y0 = w[start, +N), y1 = w[start + N/2, +N)
-                const float2* src = in_u + P.rx_base + sy.sigma + tid;
+                const float2* src = in_u + P.rx_base + sy.sigma + gtid;
 #pragma unroll
                 for (int mm = 0; mm < 24; ++mm) {
                     const float2 val = __ldg(&src[T * mm]);
@@ -596,22 +646,23 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) rx_kernel(const KP
                     if (mm >= 8) v[1][mm - 8] = val;
                 }
             }
-            __syncthreads();  // previous symbol's subband stage no longer reads spec
+            team_sync<G>(g, TT);  // previous symbol's subband stage no longer reads spec
             {
                 float2* const bufs[2] = {spec0, spec1};
-                if (!(P.dbg_skip & 2)) team_fft<N, T, kPPT, -1, 2, true>(v, bufs, P.tw, 1, tid, act);
+                if (!(P.dbg_skip & 2))
+                    team_fft<N, T, kPPT, -1, 2, true>(v, bufs, P.tw, 1, gtid, act, G == 1 ? 0 : 1 + g, TT);
             }
-            __syncthreads();
+            team_sync<G>(g, TT);
             if (act) {
 #pragma unroll
                 for (int m = 0; m < kPPT; ++m) {
-                    spec0[tid + T * m] = v[0][m];
-                    spec1[tid + T * m] = v[1][m];
+                    spec0[gtid + T * m] = v[0][m];
+                    spec1[gtid + T * m] = v[1][m];
                 }
             }
-            __syncthreads();
+            team_sync<G>(g, TT);
             if (!(P.dbg_skip & 1))
-                rx_short_all<N, LU>(P, sy, spec0, spec1, out_u + (long long)n * P.row_len, scr, stw);
+                rx_short_all<N, LU>(P, tm, sy, spec0, spec1, out_u + (long long)n * P.row_len, S.scr, S.stw);
         }
     }
 }

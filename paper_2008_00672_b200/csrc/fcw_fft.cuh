@@ -158,12 +158,18 @@ FCW_DI void fft_reg(float2 (&x)[L]) {
 }
 
 // ------------------------------------------------------------ team barriers
+// CTA-scope teams sync on barrier 0 (the whole block) or, for a sub-team, on
+// named barrier bar_id over bar_n threads; warp teams use __syncwarp.
 template <bool CTA>
-FCW_DI void team_bar() {
-    if constexpr (CTA)
-        __syncthreads();
-    else
+FCW_DI void team_bar(int bar_id, int bar_n) {
+    if constexpr (CTA) {
+        if (bar_id == 0)
+            __syncthreads();
+        else
+            asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(bar_n) : "memory");
+    } else {
         __syncwarp();
+    }
 }
 
 FCW_DI int spad(int e) { return e + (e >> 4); }
@@ -202,7 +208,7 @@ FCW_DI void twiddle_powers(float2 (&w)[R], const float2* tw, int e0) {
 // One Stockham pass (and the remaining ones, recursively).
 template <int n, int T, int PPT, int SIGN, int NF, bool CTA, int NS>
 FCW_DI void team_pass(float2 (&v)[NF][PPT], float2* const* buf, const float2* __restrict__ tw,
-                      int ts, int t, bool act) {
+                      int ts, int t, bool act, int bar_id, int bar_n) {
     constexpr int R0 = PPT < 16 ? PPT : 16;
     constexpr int REM = n / NS;
     constexpr int R = REM < R0 ? REM : R0;
@@ -236,7 +242,7 @@ FCW_DI void team_pass(float2 (&v)[NF][PPT], float2* const* buf, const float2* __
         }
     }
     if constexpr (!LAST) {
-        team_bar<CTA>();
+        team_bar<CTA>(bar_id, bar_n);
         if (act) {
 #pragma unroll
             for (int i = 0; i < NB; ++i) {
@@ -248,14 +254,14 @@ FCW_DI void team_pass(float2 (&v)[NF][PPT], float2* const* buf, const float2* __
                     for (int k = 0; k < R; ++k) buf[f][spad(base + k * NS)] = v[f][i + k * NB];
             }
         }
-        team_bar<CTA>();
+        team_bar<CTA>(bar_id, bar_n);
         if (act) {
 #pragma unroll
             for (int f = 0; f < NF; ++f)
 #pragma unroll
                 for (int m = 0; m < PPT; ++m) v[f][m] = buf[f][spad(t + T * m)];
         }
-        team_pass<n, T, PPT, SIGN, NF, CTA, NS * R>(v, buf, tw, ts, t, act);
+        team_pass<n, T, PPT, SIGN, NF, CTA, NS * R>(v, buf, tw, ts, t, act, bar_id, bar_n);
     }
 }
 
@@ -265,7 +271,7 @@ FCW_DI void team_pass(float2 (&v)[NF][PPT], float2* const* buf, const float2* __
 // input's source memory once it has been read into v.
 template <int n, int T, int PPT, int SIGN, int NF, bool CTA>
 FCW_DI void team_fft(float2 (&v)[NF][PPT], float2* const* buf, const float2* __restrict__ tw, int ts,
-                     int t, bool act) {
+                     int t, bool act, int bar_id = 0, int bar_n = 0) {
     static_assert(n == T * PPT, "team_fft: n != T*PPT");
     if constexpr (n == 1) return;
     if constexpr (T == 1) {
@@ -274,7 +280,7 @@ FCW_DI void team_fft(float2 (&v)[NF][PPT], float2* const* buf, const float2* __r
             for (int f = 0; f < NF; ++f) fft_reg<PPT, SIGN>(v[f]);
         }
     } else {
-        team_pass<n, T, PPT, SIGN, NF, CTA, 1>(v, buf, tw, ts, t, act);
+        team_pass<n, T, PPT, SIGN, NF, CTA, 1>(v, buf, tw, ts, t, act, bar_id, bar_n);
     }
 }
 

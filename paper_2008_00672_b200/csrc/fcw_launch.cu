@@ -1,6 +1,10 @@
 // Launch configuration and the K-GEN generator kernel.
 #include <algorithm>
+#include <cstdint>
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include "fcw_device.cuh"
 
@@ -56,31 +60,84 @@ int scratch_stride(const Plan& p, int LU, bool tx, bool rx_direct) {
 
 int stab_len(const Plan& p) { return p.Lmax >= 64 ? p.Lmax : 0; }
 
+// Independent teams per CTA (must match teams_per_cta<N> in fcw_device.cuh).
+int teams(const Plan& p) { return (p.N >= 512 && p.N <= 4096) ? 4096 / p.N : 1; }
+
 size_t smem_bytes(const Plan& p, bool tx, bool rx_direct) {
     const int LU = uniform_L(p);
-    const size_t f2 = 2 * (size_t)spec_stride(p) + (size_t)kWarps * scratch_stride(p, LU, tx, rx_direct) +
-                      stab_len(p) + 1 /* s_item */;
+    const size_t f2 = 2 * (size_t)teams(p) * spec_stride(p) +
+                      (size_t)kWarps * scratch_stride(p, LU, tx, rx_direct) + stab_len(p) +
+                      (teams(p) + 1) / 2 /* s_item slots */;
     return f2 * sizeof(float2);
 }
 
 // Persistent launch: as many CTAs as can be resident, each pulling work items
 // (unit, run of symbols) from a counter.  The counter and the TX carry buffers
 // are per-launch stream-ordered scratch, so concurrent launches never share.
-cudaError_t launch_one(KernelFn k, size_t smem, KParams& kp, bool tx, int N, cudaStream_t st) {
-    if (!k) return cudaErrorInvalidValue;
+// Per-device stream-ordered pool that keeps freed memory (release threshold
+// = max): the per-launch scratch is then a sub-microsecond pool hit instead of
+// an OS allocation after every synchronisation.
+cudaError_t scratch_pool(int dev, cudaMemPool_t* out) {
+    static std::mutex mu;
+    static std::map<int, cudaMemPool_t> pools;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = pools.find(dev);
+    if (it != pools.end()) {
+        *out = it->second;
+        return cudaSuccess;
+    }
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t pool;
+    cudaError_t e = cudaMemPoolCreate(&pool, &props);
+    if (e != cudaSuccess) return e;
+    uint64_t keep = UINT64_MAX;
+    e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    if (e != cudaSuccess) return e;
+    pools[dev] = pool;
+    *out = pool;
+    return cudaSuccess;
+}
+
+// Resident CTAs per SM for (kernel, smem, device); sets the dynamic-SMEM
+// attribute once.  Cached: the queries cost host time on every launch.
+cudaError_t resident_per_sm(KernelFn k, size_t smem, int dev, int* per_sm) {
+    static std::mutex mu;
+    static std::map<std::pair<std::pair<const void*, size_t>, int>, int> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    const auto key = std::make_pair(std::make_pair(reinterpret_cast<const void*>(k), smem), dev);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+        *per_sm = it->second;
+        return cudaSuccess;
+    }
     cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(k),
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, reinterpret_cast<const void*>(k), kThreads, smem);
+    if (e != cudaSuccess) return e;
+    cache[key] = *per_sm;
+    return cudaSuccess;
+}
+
+cudaError_t launch_one(KernelFn k, size_t smem, KParams& kp, bool tx, int N, int G, cudaStream_t st) {
+    if (!k) return cudaErrorInvalidValue;
     int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(k), kThreads, smem);
+    e = resident_per_sm(k, smem, dev, &per_sm);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
-    const int grid = std::max(1, std::min(kp.n_items, per_sm * sms));
-    const size_t carry_bytes = tx ? (size_t)grid * (N / 2) * sizeof(float2) : 0;
+    const int grid = std::max(1, std::min((kp.n_items + G - 1) / G, per_sm * sms));
+    const size_t carry_bytes = tx ? (size_t)grid * G * (N / 2) * sizeof(float2) : 0;
+    cudaMemPool_t pool;
+    e = scratch_pool(dev, &pool);
+    if (e != cudaSuccess) return e;
     void* scratch = nullptr;
-    e = cudaMallocAsync(&scratch, 256 + carry_bytes, st);
+    e = cudaMallocFromPoolAsync(&scratch, 256 + carry_bytes, pool, st);
     if (e != cudaSuccess) return e;
     kp.item_counter = static_cast<int*>(scratch);
     kp.carry = tx ? reinterpret_cast<float2*>(static_cast<char*>(scratch) + 256) : nullptr;
@@ -133,7 +190,7 @@ cudaError_t launch_tx(const Plan& p, KParams& kp, int S, cudaStream_t st) {
     const int LU = uniform_L(p);
     kp.scratch_stride = scratch_stride(p, LU, true, false);
     kp.n_items = S * kp.nchunks;
-    return launch_one(pick(p.N, LU).tx, smem_bytes(p, true, false), kp, true, p.N, st);
+    return launch_one(pick(p.N, LU).tx, smem_bytes(p, true, false), kp, true, p.N, teams(p), st);
 }
 
 cudaError_t launch_rx(const Plan& p, KParams& kp, int S, cudaStream_t st) {
@@ -141,7 +198,7 @@ cudaError_t launch_rx(const Plan& p, KParams& kp, int S, cudaStream_t st) {
     const bool direct = !kp.fused;
     kp.scratch_stride = scratch_stride(p, LU, false, direct);
     kp.n_items = S * kp.nchunks;
-    return launch_one(pick(p.N, LU).rx, smem_bytes(p, false, direct), kp, false, p.N, st);
+    return launch_one(pick(p.N, LU).rx, smem_bytes(p, false, direct), kp, false, p.N, teams(p), st);
 }
 
 // K-GEN: one thread per QAM symbol; splitmix64 is counter-based, so draw j of
