@@ -501,8 +501,17 @@ FCW_DI int next_item(const KParams& P, int* s_item, int g, int gtid, int nthr) {
 // warp scratch per warp, the short twiddle table and G item slots.
 struct Smem {
     float2 *spec0, *spec1, *scr, *stw;
+    float2* ltw;  // two-level long-transform twiddles: W_N^i (64), W_N^(64 h) (N/64)
     int* s_item;
 };
+
+// Two-level long-transform twiddle table in SMEM for N >= 1024 (no global
+// loads inside the long transform); smaller N read the plan table directly.
+template <int N>
+constexpr int long_twl() {
+    return N >= 1024 ? 6 : 0;
+}
+constexpr int kLtwLen = 64 + 4096 / 64;
 template <int G>
 FCW_DI Smem smem_layout(const KParams& P, int g) {
     extern __shared__ float4 smem_raw[];
@@ -513,7 +522,8 @@ FCW_DI Smem smem_layout(const KParams& P, int g) {
     float2* rest = sm + 2 * G * P.spec_stride;
     s.scr = rest + (threadIdx.x >> 5) * P.scratch_stride;
     s.stw = rest + kWarps * P.scratch_stride;
-    s.s_item = reinterpret_cast<int*>(s.stw + P.stab_len) + g;
+    s.ltw = s.stw + P.stab_len;
+    s.s_item = reinterpret_cast<int*>(s.ltw + kLtwLen) + g;
     return s;
 }
 
@@ -532,6 +542,8 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) tx_kernel(const KP
     // (L2-resident) buffer: written and read back by this team only.
     float2* carry = P.carry + ((long long)blockIdx.x * G + g) * (N / 2);
     for (int i = tid; i < P.stab_len; i += kThreads) S.stw[i] = __ldg(&P.tw[i * (N / P.stab_len)]);
+    if constexpr (long_twl<N>() > 0)
+        for (int i = tid; i < 64 + N / 64; i += kThreads) S.ltw[i] = __ldg(&P.tw[i < 64 ? i : 64 * (i - 64)]);
     __syncthreads();
 
     for (int item = next_item<G>(P, S.s_item, g, gtid, TT); item < P.n_items;
@@ -584,7 +596,8 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) tx_kernel(const KP
             {
                 float2* const bufs[2] = {spec0, spec1};
                 if (!(P.dbg_skip & 2))
-                    team_fft<N, T, kPPT, +1, 2, true>(v, bufs, P.tw, 1, gtid, act, G == 1 ? 0 : 1 + g, TT);
+                    team_fft<N, T, kPPT, +1, 2, true, long_twl<N>()>(v, bufs, long_twl<N>() ? S.ltw : P.tw, 1, gtid, act,
+                                                                    G == 1 ? 0 : 1 + g, TT);
             }
             team_sync<G>(g, TT);  // every thread has read its carry before it is overwritten
             // symbol-wise overlap-add: block 0 at 0, block 1 at N/2, carry from n-1
@@ -621,6 +634,8 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) rx_kernel(const KP
     const Smem S = smem_layout<G>(P, g);
     float2 *spec0 = S.spec0, *spec1 = S.spec1;
     for (int i = tid; i < P.stab_len; i += kThreads) S.stw[i] = __ldg(&P.tw[i * (N / P.stab_len)]);
+    if constexpr (long_twl<N>() > 0)
+        for (int i = tid; i < 64 + N / 64; i += kThreads) S.ltw[i] = __ldg(&P.tw[i < 64 ? i : 64 * (i - 64)]);
     __syncthreads();
 
     for (int item = next_item<G>(P, S.s_item, g, gtid, TT); item < P.n_items;
@@ -650,7 +665,8 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) rx_kernel(const KP
             {
                 float2* const bufs[2] = {spec0, spec1};
                 if (!(P.dbg_skip & 2))
-                    team_fft<N, T, kPPT, -1, 2, true>(v, bufs, P.tw, 1, gtid, act, G == 1 ? 0 : 1 + g, TT);
+                    team_fft<N, T, kPPT, -1, 2, true, long_twl<N>()>(v, bufs, long_twl<N>() ? S.ltw : P.tw, 1, gtid, act,
+                                                                    G == 1 ? 0 : 1 + g, TT);
             }
             team_sync<G>(g, TT);
             if (act) {

@@ -178,11 +178,16 @@ FCW_DI int spad(int e) { return e + (e >> 4); }
 // W^8e0) and at most two products each, so every power carries at most ~3 ulp
 // of rounding (a plain k-step recurrence would grow linearly in k).
 // tw is the plan table exp(-2 pi i m / N); e0 is already in table units and
-// k*e0 < N for every k < R.
-template <int R, int SIGN>
+// k*e0 < N for every k < R.  TWL > 0 selects a two-level SMEM table instead:
+// tw[0 .. 2^TWL) = W^i, tw[2^TWL + h] = W^(h 2^TWL), and W^e = hi * lo.
+template <int R, int SIGN, int TWL = 0>
 FCW_DI void twiddle_powers(float2 (&w)[R], const float2* tw, int e0) {
     auto ld = [&](int e) {
-        float2 v = tw[e];  // generic load: tw may live in SMEM or global
+        float2 v;
+        if constexpr (TWL > 0)
+            v = cmul(tw[(1 << TWL) + (e >> TWL)], tw[e & ((1 << TWL) - 1)]);
+        else
+            v = tw[e];  // generic load: tw may live in SMEM or global
         if constexpr (SIGN > 0) v.y = -v.y;
         return v;
     };
@@ -206,7 +211,7 @@ FCW_DI void twiddle_powers(float2 (&w)[R], const float2* tw, int e0) {
 }
 
 // One Stockham pass (and the remaining ones, recursively).
-template <int n, int T, int PPT, int SIGN, int NF, bool CTA, int NS>
+template <int n, int T, int PPT, int SIGN, int NF, bool CTA, int NS, int TWL>
 FCW_DI void team_pass(float2 (&v)[NF][PPT], float2* const* buf, const float2* __restrict__ tw,
                       int ts, int t, bool act, int bar_id, int bar_n) {
     constexpr int R0 = PPT < 16 ? PPT : 16;
@@ -227,7 +232,7 @@ FCW_DI void team_pass(float2 (&v)[NF][PPT], float2* const* buf, const float2* __
             if constexpr (NS > 1) {
                 const int jm = j & (NS - 1);
                 float2 wk[R];
-                twiddle_powers<R, SIGN>(wk, tw, jm * (n / (NS * R)) * ts);
+                twiddle_powers<R, SIGN, TWL>(wk, tw, jm * (n / (NS * R)) * ts);
 #pragma unroll
                 for (int k = 1; k < R; ++k)
 #pragma unroll
@@ -261,7 +266,7 @@ FCW_DI void team_pass(float2 (&v)[NF][PPT], float2* const* buf, const float2* __
 #pragma unroll
                 for (int m = 0; m < PPT; ++m) v[f][m] = buf[f][spad(t + T * m)];
         }
-        team_pass<n, T, PPT, SIGN, NF, CTA, NS * R>(v, buf, tw, ts, t, act, bar_id, bar_n);
+        team_pass<n, T, PPT, SIGN, NF, CTA, NS * R, TWL>(v, buf, tw, ts, t, act, bar_id, bar_n);
     }
 }
 
@@ -269,7 +274,7 @@ FCW_DI void team_pass(float2 (&v)[NF][PPT], float2* const* buf, const float2* __
 // thread of the block) must call it; threads with act == false only join the
 // barriers.  The buffers must hold spad(n) + 1 float2 each and may alias the
 // input's source memory once it has been read into v.
-template <int n, int T, int PPT, int SIGN, int NF, bool CTA>
+template <int n, int T, int PPT, int SIGN, int NF, bool CTA, int TWL = 0>
 FCW_DI void team_fft(float2 (&v)[NF][PPT], float2* const* buf, const float2* __restrict__ tw, int ts,
                      int t, bool act, int bar_id = 0, int bar_n = 0) {
     static_assert(n == T * PPT, "team_fft: n != T*PPT");
@@ -280,7 +285,7 @@ FCW_DI void team_fft(float2 (&v)[NF][PPT], float2* const* buf, const float2* __r
             for (int f = 0; f < NF; ++f) fft_reg<PPT, SIGN>(v[f]);
         }
     } else {
-        team_pass<n, T, PPT, SIGN, NF, CTA, 1>(v, buf, tw, ts, t, act, bar_id, bar_n);
+        team_pass<n, T, PPT, SIGN, NF, CTA, 1, TWL>(v, buf, tw, ts, t, act, bar_id, bar_n);
     }
 }
 

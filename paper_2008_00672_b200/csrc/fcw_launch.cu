@@ -67,7 +67,7 @@ size_t smem_bytes(const Plan& p, bool tx, bool rx_direct) {
     const int LU = uniform_L(p);
     const size_t f2 = 2 * (size_t)teams(p) * spec_stride(p) +
                       (size_t)kWarps * scratch_stride(p, LU, tx, rx_direct) + stab_len(p) +
-                      (teams(p) + 1) / 2 /* s_item slots */;
+                      128 /* two-level long twiddles */ + (teams(p) + 1) / 2 /* s_item slots */;
     return f2 * sizeof(float2);
 }
 
