@@ -151,10 +151,11 @@ FCW_DI void tx_short_thread(const KParams& P, const Team& tm, const SymDev& sy, 
     }
 }
 
-// Short-side TX of one subband-symbol by one warp (L >= 64), lane holds bins
-// lane + 32k.  One padded scratch buffer per warp.
+// Short-side TX of one subband-symbol by one warp (64 <= L <= 256), lane
+// holds bins lane + 32k: synchronous gather, the two block DFTs in lockstep
+// (shared twiddles, twice the ILP) over two padded scratch buffers.
 template <int N, int L>
-FCW_DI void tx_short_warp(const KParams& P, const Team& tm, const SymDev& sy, const float2* __restrict__ row,
+FCW_DI void tx_short_warp_lockstep(const KParams& P, const Team& tm, const SymDev& sy, const float2* __restrict__ row,
                           float2* spec0, float2* spec1, float2* scr, const float2* stw, int gstart, int gcount) {
     constexpr int PPT = L / 32;
     const int lane = threadIdx.x & 31;
@@ -227,35 +228,131 @@ FCW_DI void tx_short_warp(const KParams& P, const Team& tm, const SymDev& sy, co
     }
 }
 
+// 8-byte asynchronous global->SMEM copy (zero-fill when !valid); nothing is
+// held in registers while it is in flight.
+FCW_DI void cp_async8(void* smem_dst, const void* gsrc, bool valid) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(gsrc), "r"(valid ? 8 : 0)
+                 : "memory");
+}
+FCW_DI void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+FCW_DI void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// Request one subband's grid column (lane element b = lane + 32k) into the
+// warp's staging buffer.
+template <int L>
+FCW_DI void stage_grid(const KParams& P, int m, const float2* __restrict__ row, float2* stage, int lane) {
+    constexpr int PPT = L / 32;
+    const SubDev* sd = P.sub + m;
+    if (P.grid_full) {
+        const float2* g = row + sd->full_off + lane;
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) cp_async8(&stage[lane + 32 * k], g + 32 * k, true);
+    } else {
+        const float2* g = row + sd->act_off;
+        const int2* ce = P.cls + sd->cls_off + lane;
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) {
+            const int inv = (int)(short)(__ldg(&ce[32 * k]).x & 0xffff);
+            cp_async8(&stage[lane + 32 * k], inv >= 0 ? g + inv : g, inv >= 0);
+        }
+    }
+    cp_async_commit();
+}
+
+// Short-side TX of one subband-symbol by one warp (L >= 64), lane holds bins
+// lane + 32k.  One padded scratch buffer per warp plus a staging buffer that
+// receives the NEXT subband's grid column by cp.async while this one is
+// transformed (the first subband of the next symbol when `row_next` is set;
+// `staged` says this symbol's first subband was requested that way).
+template <int N, int L>
+FCW_DI void tx_short_warp(const KParams& P, const Team& tm, const SymDev& sy, const float2* __restrict__ row,
+                          const float2* __restrict__ row_next, bool staged, float2* spec0, float2* spec1,
+                          float2* scr, const float2* stw, int gstart, int gcount) {
+    constexpr int PPT = L / 32;
+    const int lane = threadIdx.x & 31;
+    const int sts = P.stab_len / L;
+    float2* const b1[1] = {scr};
+    float2* stage = scr + P.stage_off;
+    auto sub_of = [&](int i) { return P.grp_sub ? __ldg(&P.grp_sub[gstart + i]) : gstart + i; };
+    if (tm.warp >= gcount) return;
+    if (!staged) stage_grid<L>(P, sub_of(tm.warp), row, stage, lane);
+    for (int i = tm.warp; i < gcount; i += tm.nwarp) {
+        const SubDev sd = P.sub[sub_of(i)];
+        const float2 ph = cscale(tw_conj(P.tw, theta_exp<N>(sd.cmodN, sy.smodN)), sd.tx_scale);
+        float2 v[1][PPT];
+        cp_async_wait_all();
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) v[0][k] = cmul(stage[lane + 32 * k], ph);
+        __syncwarp();  // the staging buffer is free again
+        if (i + tm.nwarp < gcount)
+            stage_grid<L>(P, sub_of(i + tm.nwarp), row, stage, lane);
+        else if (row_next)
+            stage_grid<L>(P, sub_of(tm.warp), row_next, stage, lane);
+        team_fft<L, 32, PPT, +1, 1, false>(v, b1, stw, sts, lane, true);
+        const int lcp = sy.cp >> sd.logI;
+        float2 uu[2][PPT];  // block-0 / block-1 DFT inputs (L/4 is a multiple of 32: register renames)
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) {
+            const int e = lane + 32 * k;
+            const bool in0 = (e >= L / 4 - lcp) && (e < 3 * L / 4);
+            const bool in1 = (e >= L / 4) && (e < 3 * L / 4);
+            uu[0][k] = in0 ? v[0][(k - PPT / 4 + PPT) % PPT] : zero2();
+            uu[1][k] = in1 ? v[0][(k + PPT / 4) % PPT] : zero2();
+        }
+        const int2* ce = P.cls + sd.cls_off + lane;
+        const int qbase = sd.c - L / 2 + lane, ext0 = N + sd.ext_base;
+        const float bp1 = sd.bp1;
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            float2 (&u)[1][PPT] = *reinterpret_cast<float2(*)[1][PPT]>(&uu[r]);
+            team_fft<L, 32, PPT, -1, 1, false>(u, b1, stw, sts, lane, true);
+            float2* spec = r == 0 ? spec0 : spec1;
+            const float sgn = r == 0 ? 1.f : bp1;
+            static_for<PPT>([&](auto kc) {
+                constexpr int K = decltype(kc)::value;
+                const BinW e = bin_warp<N, L, K>(__ldg(&ce[32 * K]), qbase, ext0);
+                if (e.dest >= 0) spec[e.dest] = cscale(uu[r][K], e.w * sgn);
+            });
+        }
+    }
+}
+
 template <int N, int L>
 FCW_DI void tx_short_one(const KParams& P, const Team& tm, const SymDev& sy, const float2* __restrict__ row,
-                         float2* spec0, float2* spec1, float2* scr, const float2* stw, int gs, int gc) {
+                         const float2* __restrict__ row_next, bool staged, float2* spec0, float2* spec1,
+                         float2* scr, const float2* stw, int gs, int gc) {
     if constexpr (L <= N) {
         if constexpr (L <= 32)
             tx_short_thread<N, L>(P, tm, sy, row, spec0, spec1, gs, gc);
+        else if constexpr (L <= 256)
+            tx_short_warp_lockstep<N, L>(P, tm, sy, row, spec0, spec1, scr, stw, gs, gc);
         else
-            tx_short_warp<N, L>(P, tm, sy, row, spec0, spec1, scr, stw, gs, gc);
+            tx_short_warp<N, L>(P, tm, sy, row, row_next, staged, spec0, spec1, scr, stw, gs, gc);
     }
 }
 
 template <int N, int LU>
 FCW_DI void tx_short_all(const KParams& P, const Team& tm, const SymDev& sy, const float2* __restrict__ row,
-                         float2* spec0, float2* spec1, float2* scr, const float2* stw) {
+                         const float2* __restrict__ row_next, bool staged, float2* spec0, float2* spec1,
+                         float2* scr, const float2* stw) {
     if constexpr (LU > 0) {
-        tx_short_one<N, LU>(P, tm, sy, row, spec0, spec1, scr, stw, 0, P.M);
+        // uniform L: the next symbol's first subband is staged across calls
+        tx_short_one<N, LU>(P, tm, sy, row, row_next, staged, spec0, spec1, scr, stw, 0, P.M);
     } else {
         for (int g = 0; g < P.n_groups; ++g) {
             const int gs = P.grp_start[g], gc = P.grp_count[g];
             switch (P.grp_L[g]) {
-                case 4: tx_short_one<N, 4>(P, tm, sy, row, spec0, spec1, scr, stw, gs, gc); break;
-                case 8: tx_short_one<N, 8>(P, tm, sy, row, spec0, spec1, scr, stw, gs, gc); break;
-                case 16: tx_short_one<N, 16>(P, tm, sy, row, spec0, spec1, scr, stw, gs, gc); break;
-                case 32: tx_short_one<N, 32>(P, tm, sy, row, spec0, spec1, scr, stw, gs, gc); break;
-                case 64: tx_short_one<N, 64>(P, tm, sy, row, spec0, spec1, scr, stw, gs, gc); break;
-                case 128: tx_short_one<N, 128>(P, tm, sy, row, spec0, spec1, scr, stw, gs, gc); break;
-                case 256: tx_short_one<N, 256>(P, tm, sy, row, spec0, spec1, scr, stw, gs, gc); break;
-                case 512: tx_short_one<N, 512>(P, tm, sy, row, spec0, spec1, scr, stw, gs, gc); break;
-                case 1024: tx_short_one<N, 1024>(P, tm, sy, row, spec0, spec1, scr, stw, gs, gc); break;
+                case 4: tx_short_one<N, 4>(P, tm, sy, row, nullptr, false, spec0, spec1, scr, stw, gs, gc); break;
+                case 8: tx_short_one<N, 8>(P, tm, sy, row, nullptr, false, spec0, spec1, scr, stw, gs, gc); break;
+                case 16: tx_short_one<N, 16>(P, tm, sy, row, nullptr, false, spec0, spec1, scr, stw, gs, gc); break;
+                case 32: tx_short_one<N, 32>(P, tm, sy, row, nullptr, false, spec0, spec1, scr, stw, gs, gc); break;
+                case 64: tx_short_one<N, 64>(P, tm, sy, row, nullptr, false, spec0, spec1, scr, stw, gs, gc); break;
+                case 128: tx_short_one<N, 128>(P, tm, sy, row, nullptr, false, spec0, spec1, scr, stw, gs, gc); break;
+                case 256: tx_short_one<N, 256>(P, tm, sy, row, nullptr, false, spec0, spec1, scr, stw, gs, gc); break;
+                case 512: tx_short_one<N, 512>(P, tm, sy, row, nullptr, false, spec0, spec1, scr, stw, gs, gc); break;
+                case 1024: tx_short_one<N, 1024>(P, tm, sy, row, nullptr, false, spec0, spec1, scr, stw, gs, gc); break;
                 default: break;
             }
         }
@@ -561,7 +658,9 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) tx_kernel(const KP
             team_sync<G>(g, TT);  // previous symbol's transform no longer reads spec
             if (gtid == 0 && n + 1 < n1) prefetch_l2(in_u + (long long)(n + 1) * P.row_len, 8LL * P.row_len);
             if (!(P.dbg_skip & 1))
-                tx_short_all<N, LU>(P, tm, sy, in_u + (long long)n * P.row_len, spec0, spec1, S.scr, S.stw);
+                tx_short_all<N, LU>(P, tm, sy, in_u + (long long)n * P.row_len,
+                                    n + 1 < n1 ? in_u + (long long)(n + 1) * P.row_len : nullptr, n > nfirst,
+                                    spec0, spec1, S.scr, S.stw);
             team_sync<G>(g, TT);
             // secondary contributions of shared transition bins, in rank order
             for (int l = 0; l < P.n_lvl; ++l) {

@@ -53,6 +53,7 @@ struct KParams {
     int spec_stride;  // float2 per block spectrum in SMEM (>= N + n_ext, >= N + N/16)
     int scratch_stride;  // float2 per warp scratch
     int stab_len;        // entries of the SMEM short-transform twiddle table (plan Lmax)
+    int stage_off;       // TX: offset of the cp.async grid staging buffer in a warp's scratch
     int row_len;
     int grid_full;
     int fused;

@@ -51,11 +51,16 @@ int spec_stride(const Plan& p) {
 
 // Warp scratch: one padded buffer of the largest warp-path L, two where a path
 // transforms both blocks at once (TX; direct RX at L = 64 and generic plans).
+// TX: two FFT buffers (lockstep block DFTs for L <= 256; for L >= 512 the
+// second holds the cp.async staging of the next subband's grid values);
+// RX: one buffer, two where the direct path needs both blocks' short outputs
+// at once (L = 64, generic plans).
+int scratch_one(const Plan& p) { return (p.Lmax + p.Lmax / 16 + 2 + 1) & ~1; }
 int scratch_stride(const Plan& p, int LU, bool tx, bool rx_direct) {
     if (p.Lmax < 64) return 0;
-    const int one = (p.Lmax + p.Lmax / 16 + 2 + 1) & ~1;
-    const bool two = tx || (rx_direct && (LU == 0 || LU == 64 || p.Lmax == 64));
-    return two ? 2 * one : one;
+    if (tx) return 2 * scratch_one(p);
+    const bool two = rx_direct && (LU == 0 || LU == 64 || p.Lmax == 64);
+    return two ? 2 * scratch_one(p) : scratch_one(p);
 }
 
 int stab_len(const Plan& p) { return p.Lmax >= 64 ? p.Lmax : 0; }
@@ -179,6 +184,7 @@ void fill_common(const Plan& p, KParams& kp) {
     kp.zero_list = p.d_zero;
     kp.tw = p.d_tw;
     kp.stab_len = stab_len(p);
+    kp.stage_off = p.Lmax >= 64 ? scratch_one(p) : 0;
     const char* dbg = std::getenv("FCW_DEBUG_SKIP");
     kp.dbg_skip = dbg ? std::atoi(dbg) : 0;
 }
