@@ -174,6 +174,21 @@ FCW_DI void team_bar(int bar_id, int bar_n) {
 
 FCW_DI int spad(int e) { return e + (e >> 4); }
 
+// SMEM slot of Stockham element e for a team FFT: one pad slot per 16 is
+// conflict-free for radix-16 schedules (and NS = 1); the warp FFTs with 8 or 4
+// points per lane (L = 256, 128) use an XOR swizzle instead, which is
+// conflict-free for all of their passes (checked exhaustively, 8-byte
+// accesses in 16-lane wavefronts) and needs no padding.
+template <int T, int PPT>
+FCW_DI int saddr(int e) {
+    if constexpr (T == 32 && PPT == 8)
+        return e ^ ((e >> 3) & 15);
+    else if constexpr (T == 32 && PPT == 4)
+        return e ^ ((e >> 2) & 15);
+    else
+        return spad(e);
+}
+
 // w[k] = W^(k*e0) for k < R from log2(R) table loads (W^e0, W^2e0, W^4e0,
 // W^8e0) and at most two products each, so every power carries at most ~3 ulp
 // of rounding (a plain k-step recurrence would grow linearly in k).
@@ -256,7 +271,7 @@ FCW_DI void team_pass(float2 (&v)[NF][PPT], float2* const* buf, const float2* __
 #pragma unroll
                 for (int f = 0; f < NF; ++f)
 #pragma unroll
-                    for (int k = 0; k < R; ++k) buf[f][spad(base + k * NS)] = v[f][i + k * NB];
+                    for (int k = 0; k < R; ++k) buf[f][saddr<T, PPT>(base + k * NS)] = v[f][i + k * NB];
             }
         }
         team_bar<CTA>(bar_id, bar_n);
@@ -264,7 +279,7 @@ FCW_DI void team_pass(float2 (&v)[NF][PPT], float2* const* buf, const float2* __
 #pragma unroll
             for (int f = 0; f < NF; ++f)
 #pragma unroll
-                for (int m = 0; m < PPT; ++m) v[f][m] = buf[f][spad(t + T * m)];
+                for (int m = 0; m < PPT; ++m) v[f][m] = buf[f][saddr<T, PPT>(t + T * m)];
         }
         team_pass<n, T, PPT, SIGN, NF, CTA, NS * R, TWL>(v, buf, tw, ts, t, act, bar_id, bar_n);
     }
