@@ -594,6 +594,26 @@ FCW_DI int next_item(const KParams& P, int* s_item, int g, int gtid, int nthr) {
     return *s_item;
 }
 
+// Work-item source that hides the counter's round trip: the id of the item
+// after the current one is requested when the current one starts (request)
+// and published through SMEM when it ends (next).  Every item runs at least
+// one team barrier, so thread 0's next publish never races the reads.
+template <int G>
+struct ItemQueue {
+    int* s;
+    int g, gtid, nthr;
+    int pending;
+    FCW_DI int first(const KParams& P) { return next_item<G>(P, s, g, gtid, nthr); }
+    FCW_DI void request(const KParams& P) {
+        if (gtid == 0) pending = atomicAdd(P.item_counter, 1);
+    }
+    FCW_DI int next() {
+        if (gtid == 0) *s = pending;
+        team_sync<G>(g, nthr);
+        return *s;
+    }
+};
+
 // Shared layout of both kernels' SMEM: G teams x {spec0, spec1}, then one
 // warp scratch per warp, the short twiddle table and G item slots.
 struct Smem {
@@ -643,8 +663,9 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) tx_kernel(const KP
         for (int i = tid; i < 64 + N / 64; i += kThreads) S.ltw[i] = __ldg(&P.tw[i < 64 ? i : 64 * (i - 64)]);
     __syncthreads();
 
-    for (int item = next_item<G>(P, S.s_item, g, gtid, TT); item < P.n_items;
-         item = next_item<G>(P, S.s_item, g, gtid, TT)) {
+    ItemQueue<G> q{S.s_item, g, gtid, TT, 0};
+    for (int item = q.first(P); item < P.n_items; item = q.next()) {
+        q.request(P);
         const int unit = item / P.nchunks;
         const int n0 = (item % P.nchunks) * P.chunk;
         const int n1 = min(P.B, n0 + P.chunk);
@@ -737,8 +758,9 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) rx_kernel(const KP
         for (int i = tid; i < 64 + N / 64; i += kThreads) S.ltw[i] = __ldg(&P.tw[i < 64 ? i : 64 * (i - 64)]);
     __syncthreads();
 
-    for (int item = next_item<G>(P, S.s_item, g, gtid, TT); item < P.n_items;
-         item = next_item<G>(P, S.s_item, g, gtid, TT)) {
+    ItemQueue<G> q{S.s_item, g, gtid, TT, 0};
+    for (int item = q.first(P); item < P.n_items; item = q.next()) {
+        q.request(P);
         const int unit = item / P.nchunks;
         const int n0 = (item % P.nchunks) * P.chunk;
         const int n1 = min(P.B, n0 + P.chunk);
