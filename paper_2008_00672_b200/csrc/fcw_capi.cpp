@@ -70,33 +70,32 @@ long long cp_partial(const std::vector<int>& cp, int n) {
     return s;
 }
 
-// Symbols per work item.  Items are handed out dynamically to the resident
-// CTAs (~2 per SM); aim for ~16 items per CTA on TX (each item recomputes one
-// symbol to obtain its incoming carry) and ~32 on RX (no recompute).
-int pick_chunk(const fcw::Plan& p, int S, bool tx) {
-    if (const char* e = std::getenv(tx ? "FCW_CHUNK_TX" : "FCW_CHUNK_RX")) {
-        const int c = std::atoi(e);
-        if (c > 0) return std::min(c, p.B);
+// Work distribution of one launch (see RunSource in fcw_device.cuh):
+// static balanced ranges when each resident team gets few symbols (many GPUs,
+// small batches: fewest TX run starts, +-1 symbol balance), dynamic runs of
+// `chunk` symbols at full load (absorbs CTA speed differences).  FCW_CHUNK /
+// FCW_CHUNK_TX / FCW_CHUNK_RX force dynamic mode with that run length (tests
+// use it to exercise the TX carry recompute at every run start).
+void pick_schedule(const fcw::Plan& p, int S, bool tx, fcw::KParams& kp) {
+    kp.chunk = p.B;
+    kp.dynamic = 0;
+    for (const char* name : {tx ? "FCW_CHUNK_TX" : "FCW_CHUNK_RX", "FCW_CHUNK"})
+        if (const char* e = std::getenv(name)) {
+            const int c = std::atoi(e);
+            if (c > 0) {
+                kp.chunk = std::min(c, p.B);
+                kp.dynamic = 1;
+                break;
+            }
+        }
+    const int G = (p.N >= 512 && p.N <= 4096) ? 4096 / p.N : 1;
+    const long long teams = 2LL * 148 * G;
+    const long long per_team = (long long)p.B * std::max(S, 1) / teams;
+    if (!kp.dynamic && per_team >= 200) {
+        kp.dynamic = 1;
+        kp.chunk = std::min(p.B, tx ? 28 : 16);
     }
-    if (const char* e = std::getenv("FCW_CHUNK")) {
-        const int c = std::atoi(e);
-        if (c > 0) return std::min(c, p.B);
-    }
-    const long long resident = 2LL * 148 * ((p.N >= 512 && p.N <= 4096) ? 4096 / p.N : 1);  // teams
-    const long long per_cta = tx ? 16 : 32;
-    long long c = ((long long)p.B * std::max(S, 1) + per_cta * resident - 1) / (per_cta * resident);
-    if (tx) {
-        // runs of >= 8 amortise the recomputed symbol, unless that would leave
-        // resident CTAs without work (few units): then fill the GPU first
-        long long floor_c = std::min(p.B, 8);
-        const long long fill = ((long long)p.B * std::max(S, 1) + resident - 1) / resident;
-        if ((long long)std::max(S, 1) * ((p.B + floor_c - 1) / floor_c) < resident)
-            floor_c = std::max<long long>(2, std::min(floor_c, fill));
-        c = std::max(c, floor_c);
-    }
-    c = std::min<long long>(c, p.B);
-    const long long nch = (p.B + c - 1) / c;  // rebalance run lengths
-    return (int)((p.B + nch - 1) / nch);
+    kp.nchunks = (p.B + kp.chunk - 1) / kp.chunk;
 }
 
 }  // namespace
@@ -484,7 +483,7 @@ int fcw_plan_create(fcw_plan** out, int N, double overlap, const int* cp_high, i
         delete p;
         return fail(FCW_ENOTSUP, "plan exceeds the per-CTA shared-memory envelope");
     }
-    p->chunk = pick_chunk(*p, 1, true);
+    p->chunk = p->B;
     *out = p;
     return FCW_OK;
 }
@@ -578,8 +577,8 @@ int fcw_tx(const fcw_plan* p, const void* grid, int64_t grid_stride, void* wave,
     if (wave_stride < p->Q) return fail(FCW_EINVAL, "waveform unit stride smaller than Q");
     fcw::KParams kp{};
     fcw::fill_common(*p, kp);
-    kp.chunk = pick_chunk(*p, S, true);
-    kp.nchunks = (p->B + kp.chunk - 1) / kp.chunk;
+    if ((long long)S * p->B >= (1LL << 31)) return fail(FCW_ENOTSUP, "S*B symbols per launch must be < 2^31");
+    pick_schedule(*p, S, true, kp);
     kp.row_len = row;
     kp.grid_full = (flags & FCW_GRID_FULL) ? 1 : 0;
     kp.accumulate = (flags & FCW_TX_ACCUMULATE) ? 1 : 0;
@@ -611,8 +610,8 @@ int fcw_rx(const fcw_plan* p, const void* wave, int64_t wave_stride, int64_t wav
     if (grid_stride < (int64_t)p->B * row) return fail(FCW_EINVAL, "grid unit stride too small");
     fcw::KParams kp{};
     fcw::fill_common(*p, kp);
-    kp.chunk = pick_chunk(*p, S, false);
-    kp.nchunks = (p->B + kp.chunk - 1) / kp.chunk;
+    if ((long long)S * p->B >= (1LL << 31)) return fail(FCW_ENOTSUP, "S*B symbols per launch must be < 2^31");
+    pick_schedule(*p, S, false, kp);
     kp.row_len = row;
     kp.grid_full = (flags & FCW_GRID_FULL) ? 1 : 0;
     kp.fused = (flags & FCW_RX_FUSED) ? 1 : 0;

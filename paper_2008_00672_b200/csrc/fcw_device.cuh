@@ -584,42 +584,60 @@ FCW_DI void team_sync(int g, int nthr) {
         asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(nthr) : "memory");
 }
 
-// Next work item (unit, run of symbols) for this team: dynamic scheduling
-// through one global counter keeps the tail short.
-template <int G>
-FCW_DI int next_item(const KParams& P, int* s_item, int g, int gtid, int nthr) {
-    team_sync<G>(g, nthr);  // everyone has read the previous item id
-    if (gtid == 0) *s_item = atomicAdd(P.item_counter, 1);
-    team_sync<G>(g, nthr);
-    return *s_item;
-}
+// Work distribution over the resident teams, two modes (chosen per launch):
+//  * static: the launch's S*B (unit, symbol) pairs are split into one
+//    contiguous balanced range per team, walked unit by unit (runs of at most
+//    P.chunk symbols).  Few run starts (TX recomputes one symbol per start) and
+//    +-1 symbol balance: best when each team has little work (many GPUs).
+//  * dynamic: runs of P.chunk symbols are pulled from a global counter; the
+//    next run's id is requested when a run starts, so the counter's round
+//    trip is hidden.  Absorbs speed differences between CTAs: best at full
+//    load.
+template <int G, bool DYN>
+struct RunSource {
+    int pos, hi;  // static: this team's remaining range of S*B symbols
+    int pending;  // dynamic: id of the next run (-1 before the first fetch)
 
-// Work-item source that hides the counter's round trip: the id of the item
-// after the current one is requested when the current one starts (request)
-// and published through SMEM when it ends (next).  Every item runs at least
-// one team barrier, so thread 0's next publish never races the reads.
-template <int G>
-struct ItemQueue {
-    int* s;
-    int g, gtid, nthr;
-    int pending;
-    FCW_DI int first(const KParams& P) { return next_item<G>(P, s, g, gtid, nthr); }
-    FCW_DI void request(const KParams& P) {
-        if (gtid == 0) pending = atomicAdd(P.item_counter, 1);
+    FCW_DI RunSource(const KParams& P, int g) : pos(0), hi(0), pending(-1) {
+        if constexpr (!DYN) {
+            const long long total = (long long)P.n_units * P.B;
+            const long long nt = (long long)gridDim.x * P.teams;
+            const long long t = (long long)blockIdx.x * P.teams + g;
+            pos = (int)(total * t / nt);
+            hi = (int)(total * (t + 1) / nt);
+        }
     }
-    FCW_DI int next() {
-        if (gtid == 0) *s = pending;
+
+    // Next run (unit, [n0, n1)); false when the team is done.
+    FCW_DI bool next(const KParams& P, int* s_item, int g, int gtid, int nthr, int& unit, int& n0, int& n1) {
+        if constexpr (!DYN) {
+            if (pos >= hi) return false;
+            unit = pos / P.B;
+            n0 = pos - unit * P.B;
+            n1 = min(P.B, n0 + min(P.chunk, hi - pos));
+            pos += n1 - n0;
+            return true;
+        }
+        // every run executes at least one team barrier after the previous
+        // read of *s_item, so this publish cannot race it
+        if (gtid == 0) *s_item = pending >= 0 ? pending : atomicAdd(P.item_counter, 1);
         team_sync<G>(g, nthr);
-        return *s;
+        const int item = *s_item;
+        if (item >= P.n_items) return false;
+        if (gtid == 0) pending = atomicAdd(P.item_counter, 1);  // next run, in flight
+        unit = item / P.nchunks;
+        n0 = (item - unit * P.nchunks) * P.chunk;
+        n1 = min(P.B, n0 + P.chunk);
+        return true;
     }
 };
 
 // Shared layout of both kernels' SMEM: G teams x {spec0, spec1}, then one
-// warp scratch per warp, the short twiddle table and G item slots.
+// warp scratch per warp, the short twiddle table and the long two-level table.
 struct Smem {
     float2 *spec0, *spec1, *scr, *stw;
     float2* ltw;  // two-level long-transform twiddles: W_N^i (64), W_N^(64 h) (N/64)
-    int* s_item;
+    int* s_item;  // this team's run-id slot (dynamic mode)
 };
 
 // Two-level long-transform twiddle table in SMEM for N >= 1024 (no global
@@ -644,7 +662,7 @@ FCW_DI Smem smem_layout(const KParams& P, int g) {
     return s;
 }
 
-template <int N, int LU>
+template <int N, int LU, bool DYN>
 __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) tx_kernel(const KParams P) {
     constexpr int G = teams_per_cta<N>();
     constexpr int T = N / kPPT;                  // long-transform threads per team
@@ -663,12 +681,9 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) tx_kernel(const KP
         for (int i = tid; i < 64 + N / 64; i += kThreads) S.ltw[i] = __ldg(&P.tw[i < 64 ? i : 64 * (i - 64)]);
     __syncthreads();
 
-    ItemQueue<G> q{S.s_item, g, gtid, TT, 0};
-    for (int item = q.first(P); item < P.n_items; item = q.next()) {
-        q.request(P);
-        const int unit = item / P.nchunks;
-        const int n0 = (item % P.nchunks) * P.chunk;
-        const int n1 = min(P.B, n0 + P.chunk);
+    RunSource<G, DYN> runs(P, g);
+    int unit, n0, n1;
+    while (runs.next(P, S.s_item, g, gtid, TT, unit, n0, n1)) {
         const float2* in_u = P.in + (long long)unit * P.in_stride;
         float2* out_u = P.out + (long long)unit * P.out_stride;
         const int nfirst = n0 > 0 ? n0 - 1 : 0;
@@ -742,7 +757,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) tx_kernel(const KP
     }
 }
 
-template <int N, int LU>
+template <int N, int LU, bool DYN>
 __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) rx_kernel(const KParams P) {
     constexpr int G = teams_per_cta<N>();
     constexpr int T = N / kPPT;
@@ -758,12 +773,9 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) rx_kernel(const KP
         for (int i = tid; i < 64 + N / 64; i += kThreads) S.ltw[i] = __ldg(&P.tw[i < 64 ? i : 64 * (i - 64)]);
     __syncthreads();
 
-    ItemQueue<G> q{S.s_item, g, gtid, TT, 0};
-    for (int item = q.first(P); item < P.n_items; item = q.next()) {
-        q.request(P);
-        const int unit = item / P.nchunks;
-        const int n0 = (item % P.nchunks) * P.chunk;
-        const int n1 = min(P.B, n0 + P.chunk);
+    RunSource<G, DYN> runs(P, g);
+    int unit, n0, n1;
+    while (runs.next(P, S.s_item, g, gtid, TT, unit, n0, n1)) {
         const float2* in_u = P.in + (long long)unit * P.in_stride;
         float2* out_u = P.out + (long long)unit * P.out_stride;
         if (gtid == 0) prefetch_l2(in_u + P.rx_base + P.sym[n0].sigma, 8LL * (3 * N / 2));
@@ -807,7 +819,8 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) rx_kernel(const KP
 // Dispatch tables filled by the per-N instantiation units.
 using KernelFn = void (*)(KParams);
 struct KernelPair {
-    KernelFn tx, rx;
+    KernelFn tx, rx;        // static balanced ranges
+    KernelFn tx_d, rx_d;    // dynamic runs
 };
 
 }  // namespace fcw

@@ -48,8 +48,11 @@ struct SymDev {
 // Kernel parameter block (passed by value).
 struct KParams {
     int N, B, M;
-    int chunk, nchunks;
-    int n_items;         // S * nchunks work items, handed out through item_counter
+    int chunk;           // max symbols per run (a TX run recomputes the symbol before it)
+    int n_units;         // S: units of this launch
+    int teams;           // teams per CTA (teams_per_cta<N>)
+    int dynamic;         // 1: runs pulled from item_counter; 0: static balanced ranges
+    int n_items, nchunks;  // dynamic mode: S * nchunks runs of `chunk` symbols
     int spec_stride;  // float2 per block spectrum in SMEM (>= N + n_ext, >= N + N/16)
     int scratch_stride;  // float2 per warp scratch
     int stab_len;        // entries of the SMEM short-transform twiddle table (plan Lmax)
@@ -78,8 +81,8 @@ struct KParams {
     const float2* tw;    // [N] exp(-2 pi i k / N)
     const float2* in;
     float2* out;
-    int* item_counter;   // per-launch scratch: dynamic work counter
-    float2* carry;       // per-launch scratch: gridDim.x * N/2 TX carry buffers
+    int* item_counter;   // per-launch scratch: dynamic run counter
+    float2* carry;       // per-launch scratch: gridDim.x * teams * N/2 TX carry buffers
 };
 
 struct Plan {

@@ -6,7 +6,8 @@
 
 #define FCW_SPEC(NN, LL) \
     case LL:             \
-        return KernelPair{tx_kernel<NN, LL>, rx_kernel<NN, LL>};
+        return KernelPair{tx_kernel<NN, LL, false>, rx_kernel<NN, LL, false>, tx_kernel<NN, LL, true>, \
+                          rx_kernel<NN, LL, true>};
 
 // Generic (mixed-L) kernel plus uniform-L specialisations for the common sizes.
 #define FCW_KERNELS_FULL(NN)                                                   \
@@ -19,9 +20,14 @@
             FCW_SPEC(NN, 256)                                                  \
             FCW_SPEC(NN, 512)                                                  \
             FCW_SPEC(NN, 1024)                                                 \
-            default: return KernelPair{tx_kernel<NN, 0>, rx_kernel<NN, 0>};    \
+            default:                                                           \
+                return KernelPair{tx_kernel<NN, 0, false>, rx_kernel<NN, 0, false>, tx_kernel<NN, 0, true>, \
+                                  rx_kernel<NN, 0, true>};                     \
         }                                                                      \
     }
 
 #define FCW_KERNELS_GENERIC(NN) \
-    KernelPair kernels_n##NN(int) { return KernelPair{tx_kernel<NN, 0>, rx_kernel<NN, 0>}; }
+    KernelPair kernels_n##NN(int) {                                                                  \
+        return KernelPair{tx_kernel<NN, 0, false>, rx_kernel<NN, 0, false>, tx_kernel<NN, 0, true>, \
+                          rx_kernel<NN, 0, true>};                                                  \
+    }

@@ -33,7 +33,7 @@ KernelPair pick(int N, int LU) {
         case 1024: return kernels_n1024(LU);
         case 2048: return kernels_n2048(LU);
         case 4096: return kernels_n4096(LU);
-        default: return KernelPair{nullptr, nullptr};
+        default: return KernelPair{nullptr, nullptr, nullptr, nullptr};
     }
 }
 
@@ -72,13 +72,13 @@ size_t smem_bytes(const Plan& p, bool tx, bool rx_direct) {
     const int LU = uniform_L(p);
     const size_t f2 = 2 * (size_t)teams(p) * spec_stride(p) +
                       (size_t)kWarps * scratch_stride(p, LU, tx, rx_direct) + stab_len(p) +
-                      128 /* two-level long twiddles */ + (teams(p) + 1) / 2 /* s_item slots */;
+                      128 /* two-level long twiddles */ + (teams(p) + 1) / 2 /* run-id slots */;
     return f2 * sizeof(float2);
 }
 
-// Persistent launch: as many CTAs as can be resident, each pulling work items
-// (unit, run of symbols) from a counter.  The counter and the TX carry buffers
-// are per-launch stream-ordered scratch, so concurrent launches never share.
+// Persistent launch: as many CTAs as can be resident; each team owns a static
+// balanced range of the S*B symbols.  The TX carry buffers are per-launch
+// stream-ordered scratch, so concurrent launches never share them.
 // Per-device stream-ordered pool that keeps freed memory (release threshold
 // = max): the per-launch scratch is then a sub-microsecond pool hit instead of
 // an OS allocation after every synchronisation.
@@ -136,7 +136,10 @@ cudaError_t launch_one(KernelFn k, size_t smem, KParams& kp, bool tx, int N, int
     e = resident_per_sm(k, smem, dev, &per_sm);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
-    const int grid = std::max(1, std::min((kp.n_items + G - 1) / G, per_sm * sms));
+    // at most the resident CTAs; in dynamic mode no more teams than runs,
+    // in static mode no more teams than symbols
+    const long long work = kp.dynamic ? kp.n_items : (long long)kp.n_units * kp.B;
+    const int grid = (int)std::max(1LL, std::min((work + G - 1) / G, (long long)per_sm * sms));
     const size_t carry_bytes = tx ? (size_t)grid * G * (N / 2) * sizeof(float2) : 0;
     cudaMemPool_t pool;
     e = scratch_pool(dev, &pool);
@@ -146,7 +149,7 @@ cudaError_t launch_one(KernelFn k, size_t smem, KParams& kp, bool tx, int N, int
     if (e != cudaSuccess) return e;
     kp.item_counter = static_cast<int*>(scratch);
     kp.carry = tx ? reinterpret_cast<float2*>(static_cast<char*>(scratch) + 256) : nullptr;
-    e = cudaMemsetAsync(scratch, 0, sizeof(int), st);
+    e = kp.dynamic ? cudaMemsetAsync(scratch, 0, sizeof(int), st) : cudaSuccess;
     if (e == cudaSuccess) {
         void* args[] = {&kp};
         e = cudaLaunchKernel(reinterpret_cast<const void*>(k), dim3(grid), dim3(kThreads), args, smem, st);
@@ -195,16 +198,22 @@ size_t rx_smem_bytes(const Plan& p) { return smem_bytes(p, false, true); }
 cudaError_t launch_tx(const Plan& p, KParams& kp, int S, cudaStream_t st) {
     const int LU = uniform_L(p);
     kp.scratch_stride = scratch_stride(p, LU, true, false);
+    kp.n_units = S;
+    kp.teams = teams(p);
     kp.n_items = S * kp.nchunks;
-    return launch_one(pick(p.N, LU).tx, smem_bytes(p, true, false), kp, true, p.N, teams(p), st);
+    const KernelPair kp2 = pick(p.N, LU);
+    return launch_one(kp.dynamic ? kp2.tx_d : kp2.tx, smem_bytes(p, true, false), kp, true, p.N, teams(p), st);
 }
 
 cudaError_t launch_rx(const Plan& p, KParams& kp, int S, cudaStream_t st) {
     const int LU = uniform_L(p);
     const bool direct = !kp.fused;
     kp.scratch_stride = scratch_stride(p, LU, false, direct);
+    kp.n_units = S;
+    kp.teams = teams(p);
     kp.n_items = S * kp.nchunks;
-    return launch_one(pick(p.N, LU).rx, smem_bytes(p, false, direct), kp, false, p.N, teams(p), st);
+    const KernelPair kp2 = pick(p.N, LU);
+    return launch_one(kp.dynamic ? kp2.rx_d : kp2.rx, smem_bytes(p, false, direct), kp, false, p.N, teams(p), st);
 }
 
 // K-GEN: one thread per QAM symbol; splitmix64 is counter-based, so draw j of
