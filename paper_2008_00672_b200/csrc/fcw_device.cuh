@@ -102,6 +102,14 @@ FCW_DI int theta_exp(int cmodN, int smodN) {
 
 FCW_DI float2 zero2() { return make_float2(0.f, 0.f); }
 
+// Streaming read of grid data that is used once: read-only path, no L1
+// allocation, so the small L1 beside SMEM keeps the class table entries.
+FCW_DI float2 ld_stream(const float2* p) {
+    float2 v;
+    asm("ld.global.nc.L1::no_allocate.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
+    return v;
+}
+
 FCW_DI float2 grid_val(const KParams& P, const SubDev& sd, const float2* __restrict__ row, int b, int inv) {
     if (P.grid_full) return row[sd.full_off + b];
     return inv >= 0 ? row[sd.act_off + inv] : zero2();
@@ -178,10 +186,9 @@ FCW_DI void tx_short_warp_lockstep(const KParams& P, const Team& tm, const SymDe
         } else {
             const float2* g = row + sd.act_off;
 #pragma unroll
-            for (int k = 0; k < PPT; ++k) {
-                const int inv = (int)(short)(ent[k].x & 0xffff);
-                v[0][k] = inv >= 0 ? cmul(g[inv], ph) : zero2();
-            }
+            for (int k = 0; k < PPT; ++k) v[0][k] = ld_stream(g + max((int)(short)(ent[k].x & 0xffff), 0));
+#pragma unroll
+            for (int k = 0; k < PPT; ++k) v[0][k] = (short)(ent[k].x & 0xffff) >= 0 ? cmul(v[0][k], ph) : zero2();
         }
         team_fft<L, 32, PPT, +1, 1, false>(v, b1, stw, sts, lane, true);
         const int lcp = sy.cp >> sd.logI;
@@ -524,13 +531,86 @@ FCW_DI void rx_short_warp(const KParams& P, const Team& tm, const SymDev& sy, co
     }
 }
 
+// Fused RX (Eq. 30) for L = 256 by half-warps, 16 bins per lane (element
+// b = t + 16k): both short transforms radix-16 x 16, one exchange each.
+template <int N, int L>
+FCW_DI void rx_short_half(const KParams& P, const Team& tm, const SymDev& sy, const float2* spec0,
+                          const float2* spec1, float2* __restrict__ orow, float2* scr, const float2* stw,
+                          int gstart, int gcount) {
+    constexpr int TW = 16, PPT = L / TW;
+    static_assert(L == 256, "half-warp path is built for L = 256");
+    const int lane = threadIdx.x & 31, t = lane & (TW - 1), h = lane >> 4;
+    const int sts = P.stab_len / L;
+    float2* const b1[1] = {scr + h * (P.scratch_stride / 2)};
+    for (int i0 = 2 * tm.warp; i0 < gcount; i0 += 2 * tm.nwarp) {
+        const int i = i0 + h;
+        const bool act = i < gcount;
+        const int m = act ? (P.grp_sub ? __ldg(&P.grp_sub[gstart + i]) : gstart + i) : 0;
+        const SubDev sd = P.sub[m];
+        const int2* ce = P.cls + sd.cls_off + t;
+        float2 g0[1][PPT], g1[1][PPT];
+        if (act) {
+            const int qbase = sd.c - L / 2 + t;
+            const float bp1 = sd.bp1;
+            const bool odd = t & 1;
+            static_for<PPT>([&](auto kc) {
+                constexpr int K = decltype(kc)::value;
+                constexpr int KP = K ^ (L / (2 * TW));  // (t + 16K) ^ (L/2) == t + 16*KP
+                const float w = __int_as_float(__ldg(&ce[TW * K]).y);
+                const int q = (qbase + TW * KP) & (N - 1);
+                float2 a = cscale(spec0[q], w), b = cscale(spec1[q], w * bp1);
+                if (odd) b = make_float2(-b.x, -b.y);  // t = Omega_{L/2} g1
+                g1[0][K] = b;
+                g0[0][K] = mul_jpow_rt(csub(a, b), t);  // f = Omega_{-L/4}(g0 - t); b mod 4 == t mod 4
+            });
+        } else {
+#pragma unroll
+            for (int k = 0; k < PPT; ++k) g0[0][k] = g1[0][k] = zero2();
+        }
+        team_fft<L, TW, PPT, +1, 1, false>(g0, b1, stw, sts, t, act);
+#pragma unroll
+        for (int k = PPT / 2; k < PPT; ++k) g0[0][k] = zero2();  // S-hat: elements >= L/2
+        team_fft<L, TW, PPT, -1, 1, false>(g0, b1, stw, sts, t, act);
+        if (act) {
+            const float2 ph = __ldg(&P.tw[theta_exp<N>(sd.cmodN, sy.smodN)]);  // conj(theta_n)
+            const float a = sd.rx_s0 / (float)L, s = sd.rx_s0;
+            if (P.grid_full) {
+                float2* o = orow + sd.full_off + t;
+#pragma unroll
+                for (int k = 0; k < PPT; ++k) {
+                    const float2 tj = mul_jpow_rt(g1[0][k], t);
+                    o[TW * k] = cmul(make_float2(fmaf(g0[0][k].x, a, tj.x * s), fmaf(g0[0][k].y, a, tj.y * s)), ph);
+                }
+            } else {
+                float2* o = orow + sd.act_off;
+                int inv[PPT];  // all entry loads in flight before the first store
+#pragma unroll
+                for (int k = 0; k < PPT; ++k) inv[k] = (int)(short)(__ldg(&ce[TW * k]).x & 0xffff);
+#pragma unroll
+                for (int k = 0; k < PPT; ++k) {
+                    if (inv[k] >= 0) {
+                        const float2 tj = mul_jpow_rt(g1[0][k], t);
+                        o[inv[k]] = cmul(make_float2(fmaf(g0[0][k].x, a, tj.x * s), fmaf(g0[0][k].y, a, tj.y * s)), ph);
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    }
+}
+
 template <int N, int L>
 FCW_DI void rx_short_one(const KParams& P, const Team& tm, const SymDev& sy, const float2* spec0,
                          const float2* spec1, float2* orow, float2* scr, const float2* stw, int gs, int gc) {
     if constexpr (L <= N) {
         if constexpr (L <= 32)
             rx_short_thread<N, L>(P, tm, sy, spec0, spec1, orow, gs, gc);
-        else
+        else if constexpr (L == 256) {
+            if (P.fused)
+                rx_short_half<N, L>(P, tm, sy, spec0, spec1, orow, scr, stw, gs, gc);
+            else
+                rx_short_warp<N, L>(P, tm, sy, spec0, spec1, orow, scr, stw, gs, gc);
+        } else
             rx_short_warp<N, L>(P, tm, sy, spec0, spec1, orow, scr, stw, gs, gc);
     }
 }

@@ -59,7 +59,8 @@ int scratch_one(const Plan& p) { return (p.Lmax + p.Lmax / 16 + 2 + 1) & ~1; }
 int scratch_stride(const Plan& p, int LU, bool tx, bool rx_direct) {
     if (p.Lmax < 64) return 0;
     if (tx) return 2 * scratch_one(p);
-    const bool two = rx_direct && (LU == 0 || LU == 64 || p.Lmax == 64);
+    // fused L = 256 runs on half-warps: one buffer per half
+    const bool two = (rx_direct && (LU == 0 || LU == 64 || p.Lmax == 64)) || p.Lmax == 256;
     return two ? 2 * scratch_one(p) : scratch_one(p);
 }
 

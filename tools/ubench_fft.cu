@@ -29,6 +29,28 @@ __global__ void __launch_bounds__(256, 2) warp_fft_kernel(const float2* tw_g, fl
     out[blockIdx.x * 256 + threadIdx.x] = acc;
 }
 
+// Half-warp teams: each 16-lane half of a warp transforms its own FFT_L with
+// L/16 points per lane (radix-16 x 16 for L = 256: one exchange).
+template <int L>
+__global__ void __launch_bounds__(256, 2) half_fft_kernel(const float2* tw_g, float2* out, int reps) {
+    constexpr int PPT = L / 16;
+    __shared__ float2 stw[L];
+    __shared__ float2 scr[8][2][L + L / 16 + 2];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, h = lane >> 4, t = lane & 15;
+    for (int i = threadIdx.x; i < L; i += 256) stw[i] = tw_g[i];
+    __syncthreads();
+    float2 v[1][PPT];
+    for (int k = 0; k < PPT; ++k) v[0][k] = make_float2(lane * 0.001f + k, h - k * 0.5f);
+    float2* const b[1] = {scr[warp][h]};
+    for (int r = 0; r < reps; ++r) {
+        team_fft<L, 16, PPT, -1, 1, false>(v, b, stw, 1, t, true);
+        team_fft<L, 16, PPT, +1, 1, false>(v, b, stw, 1, t, true);
+    }
+    float2 acc = make_float2(0, 0);
+    for (int k = 0; k < PPT; ++k) acc = cadd(acc, v[0][k]);
+    out[blockIdx.x * 256 + threadIdx.x] = acc;
+}
+
 template <int N>
 __global__ void __launch_bounds__(256, 2) cta_fft_kernel(const float2* tw_g, float2* out, int reps) {
     constexpr int T = N / 16;
@@ -91,6 +113,12 @@ int main() {
         double ffts = (double)grid * 8 * reps * 2 * 2;
         printf("warp FFT_256 NF=2: %.3f ms, %.2f ns/FFT (GPU), %.0f cycles/FFT/SM\n", ms, ms * 1e6 / ffts,
                ms * 1e-3 * 1.965e9 * 148 / ffts);
+    }
+    {
+        float ms = timeit([&] { half_fft_kernel<256><<<grid, 256>>>(d_tw256, d_out, reps); });
+        double ffts = (double)grid * 8 * reps * 2 * 2;
+        printf("half-warp FFT_256 (16x16, 16 pts/lane): %.3f ms, %.2f ns/FFT (GPU), %.0f cycles/FFT/SM\n", ms,
+               ms * 1e6 / ffts, ms * 1e-3 * 1.965e9 * 148 / ffts);
     }
     {
         size_t smem = 2 * (N + N / 16 + 2) * 8;
