@@ -11,6 +11,9 @@ import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "lib", "libfcwave_b200.so")
+# dev-only A/B knob: load a variant built by ``build.py --variant NAME``
+if os.environ.get("FCW_LIB_VARIANT"):
+    LIB_PATH = os.path.join(HERE, "lib", f"libfcwave_b200_{os.environ['FCW_LIB_VARIANT']}.so")
 
 FCW_OK, FCW_EINVAL, FCW_ERANGE, FCW_ECUDA, FCW_ENOMEM, FCW_ENOTSUP = range(6)
 FCW_GRID_FULL = 1

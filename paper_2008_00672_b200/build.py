@@ -24,7 +24,7 @@ NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-r
               "-Xptxas", "-v", "-I", os.path.join(ROOT, "include"), "-I", CSRC]
 CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-Wall", "-Wextra", "-I", os.path.join(ROOT, "include"), "-I", CSRC]
 
-SOURCES_CU = ["fcw_launch.cu", "fcw_k_n4096.cu", "fcw_k_n2048.cu", "fcw_k_n1024.cu", "fcw_k_small.cu"]
+SOURCES_CU = ["fcw_launch.cu", "fcw_k_small.cu"] + [f"fcw_k_n{n}{g}.cu" for n in (4096, 2048, 1024) for g in "bcag"]
 SOURCES_CPP = ["fcw_capi.cpp", "fcw_host.cpp"]
 
 
@@ -88,5 +88,36 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_variant(name: str, defines: list[str], sources: list[str]) -> str:
+    """Dev-only A/B build: the default objects with `sources` recompiled under
+    extra -D `defines`, linked as lib/libfcwave_b200_<name>.so (loaded when
+    FCW_LIB_VARIANT=<name>)."""
+    build()
+    vdir = os.path.join(OUT_DIR, "obj_" + name)
+    os.makedirs(vdir, exist_ok=True)
+    objs = []
+    jobs = []
+    for s in SOURCES_CU + SOURCES_CPP:
+        base = os.path.join(OBJ_DIR, s + ".o")
+        if s in sources:
+            obj = os.path.join(vdir, s + ".o")
+            jobs.append(([_nvcc(), *ARCH, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, s),
+                          "-o", obj], obj + ".log"))
+            objs.append(obj)
+        else:
+            objs.append(base)
+    with cf.ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
+        list(ex.map(lambda j: _run(*j), jobs))
+    lib = os.path.join(OUT_DIR, f"libfcwave_b200_{name}.so")
+    _run([_nvcc(), *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", lib, *objs, "-lcudart_static", "-lrt",
+          "-lpthread", "-ldl"], os.path.join(vdir, "link.log"))
+    return lib
+
+
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    if "--variant" in sys.argv:
+        i = sys.argv.index("--variant")
+        name, defs = sys.argv[i + 1], sys.argv[i + 2].split(",") if len(sys.argv) > i + 2 else []
+        print(build_variant(name, [d for d in defs if d], ["fcw_k_n4096b.cu"]))
+    else:
+        print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

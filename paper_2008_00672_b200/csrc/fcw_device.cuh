@@ -102,6 +102,26 @@ FCW_DI int theta_exp(int cmodN, int smodN) {
 
 FCW_DI float2 zero2() { return make_float2(0.f, 0.f); }
 
+constexpr int kLtwLen = 64 + 4096 / 64;  // two-level long-transform twiddles (SMEM)
+constexpr int kTw16Len = 512;            // fft256_half per-lane twiddles (uniform L = 256 kernels)
+#ifndef FCW_TX_HALF
+#define FCW_TX_HALF 1  // TX L = 256 on half-warps (tail on whole warps) vs whole-warp lockstep
+#endif
+#ifndef FCW_RX_HYBRID
+#define FCW_RX_HYBRID 0  // fused RX L = 256: whole-warp tail round
+#endif
+#ifndef FCW_TX_DST1
+#define FCW_TX_DST1 0  // TX half-warp scatter: decode bin destinations once for both blocks
+#endif
+#ifndef FCW_TW16
+#define FCW_TW16 1
+#endif
+// The per-lane twiddle table follows the short and long twiddle tables in SMEM
+// (filled in the kernel prologue when P.tw16 is set).
+FCW_DI const float2* tw16_of(const KParams& P, const float2* stw) {
+    return FCW_TW16 ? stw + P.stab_len + kLtwLen : nullptr;
+}
+
 // Streaming read of grid data that is used once: read-only path, no L1
 // allocation, so the small L1 beside SMEM keeps the class table entries.
 FCW_DI float2 ld_stream(const float2* p) {
@@ -326,6 +346,110 @@ FCW_DI void tx_short_warp(const KParams& P, const Team& tm, const SymDev& sy, co
     }
 }
 
+// Short-side TX for L = 256 by half-warps, 16 bins per lane (element
+// b = t + 16k), radix-16 x 16 transforms with one exchange each:
+// ofdm_modulate IDFT (ofdm.cpp:97-106), the two block windows of tx_symbol
+// (fc_sync.cpp:34-84: L/4 is a multiple of 16, so the circular shifts are
+// register renames) and the two block DFTs with their known-zero halves
+// pruned (block 1 lives on [L/4, 3L/4), block 0 on [L/4 - l_cp, 3L/4)).
+template <int N, int L>
+FCW_DI void tx_short_half(const KParams& P, const Team& tm, const SymDev& sy, const float2* __restrict__ row,
+                          float2* spec0, float2* spec1, float2* scr, const float2* stw, int gstart, int gcount) {
+    constexpr int TW = 16, PPT = L / TW;
+    static_assert(L == 256, "half-warp path is built for L = 256");
+    const int lane = threadIdx.x & 31, t = lane & (TW - 1), h = lane >> 4;
+    float2* buf = scr + h * (P.scratch_stride / 2);
+    // Rounds of 2 subbands per warp while more than one per warp remain; the
+    // tail (at most one per warp) runs on whole warps, which finish a subband
+    // in fewer dependent steps (balance: 23 subbands = 16 + 7, not 16 + 16).
+    int done = 0;
+    while (gcount - done > tm.nwarp) {
+        const int i = done + 2 * tm.warp + h;
+        done += 2 * tm.nwarp;
+        const bool act = i < gcount;
+        const int m = act ? (P.grp_sub ? __ldg(&P.grp_sub[gstart + i]) : gstart + i) : gstart;
+        const SubDev sd = P.sub[m];
+        const int2* ce = P.cls + sd.cls_off + t;
+        float2 v[PPT];
+        {
+            const float2 ph = cscale(tw_conj(P.tw, theta_exp<N>(sd.cmodN, sy.smodN)), sd.tx_scale);
+            int inv[PPT];
+#pragma unroll
+            for (int k = 0; k < PPT; ++k) inv[k] = act ? (int)(short)(__ldg(&ce[TW * k]).x & 0xffff) : -1;
+            if (P.grid_full) {
+                const float2* g = row + sd.full_off + t;
+#pragma unroll
+                for (int k = 0; k < PPT; ++k) v[k] = act ? ld_stream(g + TW * k) : zero2();
+            } else {
+                const float2* g = row + sd.act_off;
+#pragma unroll
+                for (int k = 0; k < PPT; ++k) v[k] = ld_stream(g + max(inv[k], 0));
+#pragma unroll
+                for (int k = 0; k < PPT; ++k) v[k] = inv[k] >= 0 ? v[k] : zero2();
+            }
+#pragma unroll
+            for (int k = 0; k < PPT; ++k) v[k] = cmul(v[k], ph);
+        }
+        fft256_half<+1>(v, buf, stw, t, 0, tw16_of(P, stw));  // x[t + 16 m] (scales folded into ph)
+        const int lcp = sy.cp >> sd.logI;
+        const int qbase = sd.c - L / 2 + t, ext0 = N + sd.ext_base;
+#if FCW_TX_DST1
+        // destination slot and weight of each bin, decoded once for both blocks
+        int dst[PPT];
+        float wgt[PPT];
+        static_for<PPT>([&](auto kc) {
+            constexpr int K = decltype(kc)::value;
+            constexpr int KP = K ^ (PPT / 2);  // (t + 16K) ^ (L/2) == t + 16*KP
+            const int2 e = __ldg(&ce[TW * K]);
+            const int sec = e.x >> 16;
+            dst[K] = !act ? -1 : sec >= 0 ? ext0 + sec : (sec == -1 ? ((qbase + TW * KP) & (N - 1)) : -1);
+            wgt[K] = __int_as_float(e.y);
+        });
+        auto scatter = [&](float2 (&u)[PPT], float2* spec, float sgn) {
+#pragma unroll
+            for (int K = 0; K < PPT; ++K)
+                if (dst[K] >= 0) spec[dst[K]] = cscale(u[K], wgt[K] * sgn);
+        };
+#else
+        auto scatter = [&](float2 (&u)[PPT], float2* spec, float sgn) {
+            static_for<PPT>([&](auto kc) {
+                constexpr int K = decltype(kc)::value;
+                constexpr int KP = K ^ (PPT / 2);  // (t + 16K) ^ (L/2) == t + 16*KP
+                const int2 e = __ldg(&ce[TW * K]);
+                const int sec = e.x >> 16;
+                const int dest = sec >= 0 ? ext0 + sec : (sec == -1 ? ((qbase + TW * KP) & (N - 1)) : -1);
+                if (act && dest >= 0) spec[dest] = cscale(u[K], __int_as_float(e.y) * sgn);
+            });
+        };
+#endif
+        {
+            // block 0: e = t + 16 m in [L/4 - lcp, 3L/4) holds x[(e - L/4) mod L] = v[(m - 4) mod 16]
+            float2 u[PPT];
+#pragma unroll
+            for (int k = 0; k < PPT; ++k) {
+                if (k >= 4 && k < 12)
+                    u[k] = v[k - 4];
+                else if (k < 4)
+                    u[k] = (t + TW * k >= L / 4 - lcp) ? v[k + 12] : zero2();
+                else
+                    u[k] = zero2();  // k >= 12: known zero (not read)
+            }
+            fft256_half<-1, 0xF000ull>(u, buf, stw, t, 0, tw16_of(P, stw));
+            scatter(u, spec0, 1.f);
+        }
+        {
+            // block 1: e in [L/4, 3L/4) holds x[e + L/4] = v[m + 4]
+            float2 u[PPT];
+#pragma unroll
+            for (int k = 0; k < PPT; ++k) u[k] = (k >= 4 && k < 12) ? v[k + 4] : zero2();
+            fft256_half<-1, 0xF00Full>(u, buf, stw, t, 0, tw16_of(P, stw));
+            scatter(u, spec1, sd.bp1);
+        }
+    }
+    if (done < gcount)
+        tx_short_warp_lockstep<N, L>(P, tm, sy, row, spec0, spec1, scr, stw, gstart + done, gcount - done);
+}
+
 template <int N, int L>
 FCW_DI void tx_short_one(const KParams& P, const Team& tm, const SymDev& sy, const float2* __restrict__ row,
                          const float2* __restrict__ row_next, bool staged, float2* spec0, float2* spec1,
@@ -333,6 +457,8 @@ FCW_DI void tx_short_one(const KParams& P, const Team& tm, const SymDev& sy, con
     if constexpr (L <= N) {
         if constexpr (L <= 32)
             tx_short_thread<N, L>(P, tm, sy, row, spec0, spec1, gs, gc);
+        else if constexpr (L == 256 && FCW_TX_HALF)
+            tx_short_half<N, L>(P, tm, sy, row, spec0, spec1, scr, stw, gs, gc);
         else if constexpr (L <= 256)
             tx_short_warp_lockstep<N, L>(P, tm, sy, row, spec0, spec1, scr, stw, gs, gc);
         else
@@ -533,6 +659,14 @@ FCW_DI void rx_short_warp(const KParams& P, const Team& tm, const SymDev& sy, co
 
 // Fused RX (Eq. 30) for L = 256 by half-warps, 16 bins per lane (element
 // b = t + 16k): both short transforms radix-16 x 16, one exchange each.
+// Every per-bin rotation of rx_symbol_simplified (fc_sync.cpp:195-243) is a
+// lane constant here, because b = t (mod 16):
+//   f = Omega_{-L/4}(g0 - Omega_{L/2} g1) = j^t * w (S0 - (-1)^t bp1 S1):
+//     the j^t factor is folded into the IDFT's pass-2 twiddles (eoff = L/4);
+//   out = conj(theta) (a G + s j^t t) = P1 G + P2 (w S1), with
+//     P1 = a conj(theta), P2 = s bp1 (-j)^t conj(theta) per lane and subband.
+// The spectra carry a wrap-around copy of bins [0, L) at [N, N + L), so the
+// bin addresses of a subband are one base plus immediate offsets.
 template <int N, int L>
 FCW_DI void rx_short_half(const KParams& P, const Team& tm, const SymDev& sy, const float2* spec0,
                           const float2* spec1, float2* __restrict__ orow, float2* scr, const float2* stw,
@@ -540,72 +674,67 @@ FCW_DI void rx_short_half(const KParams& P, const Team& tm, const SymDev& sy, co
     constexpr int TW = 16, PPT = L / TW;
     static_assert(L == 256, "half-warp path is built for L = 256");
     const int lane = threadIdx.x & 31, t = lane & (TW - 1), h = lane >> 4;
-    const int sts = P.stab_len / L;
-    float2* const b1[1] = {scr + h * (P.scratch_stride / 2)};
-    for (int i0 = 2 * tm.warp; i0 < gcount; i0 += 2 * tm.nwarp) {
-        const int i = i0 + h;
+    float2* buf = scr + h * (P.scratch_stride / 2);
+    const float sgn_t = (t & 1) ? -1.f : 1.f;  // (-1)^b
+    int done = 0;  // half-warp rounds (while more than one subband per warp remains if FCW_RX_HYBRID)
+    while (gcount - done > (FCW_RX_HYBRID ? tm.nwarp : 0)) {
+        const int i = done + 2 * tm.warp + h;
+        done += 2 * tm.nwarp;
         const bool act = i < gcount;
-        const int m = act ? (P.grp_sub ? __ldg(&P.grp_sub[gstart + i]) : gstart + i) : 0;
+        const int m = act ? (P.grp_sub ? __ldg(&P.grp_sub[gstart + i]) : gstart + i) : gstart;
         const SubDev sd = P.sub[m];
         const int2* ce = P.cls + sd.cls_off + t;
-        float2 g0[1][PPT], g1[1][PPT];
+        const int q0 = (sd.c - L / 2 + t) & (N - 1);
+        const float2* s0 = spec0 + q0;
+        const float2* s1 = spec1 + q0;
+        const float sig = sgn_t * sd.bp1;
+        float2 f[PPT], gw[PPT];
+        static_for<PPT>([&](auto kc) {
+            constexpr int K = decltype(kc)::value;
+            constexpr int KP = K ^ (PPT / 2);  // (t + 16K) ^ (L/2) == t + 16*KP
+            const float w = __int_as_float(__ldg(&ce[TW * K]).y);
+            const float2 a = s0[TW * KP], b = s1[TW * KP];
+            gw[K] = cscale(b, w);
+            f[K] = cscale(make_float2(fmaf(-sig, b.x, a.x), fmaf(-sig, b.y, a.y)), w);
+        });
+        fft256_half<+1>(f, buf, stw, t, L / 4, tw16_of(P, stw));  // IDFT of j^t f
+        fft256_half<-1, 0xFF00ull>(f, buf, stw, t, 0, tw16_of(P, stw));  // S-hat keeps x[e], e < L/2; DFT
+        const float2 ph = __ldg(&P.tw[theta_exp<N>(sd.cmodN, sy.smodN)]);  // conj(theta_n)
+        const float2 P1 = cscale(ph, sd.rx_s0 / (float)L);
+        const float2 P2 = mul_jpow_rt(cscale(ph, sd.rx_s0 * sd.bp1), (4 - t) & 3);
+        auto outv = [&](int k) {
+            return make_float2(fmaf(f[k].x, P1.x, fmaf(-f[k].y, P1.y, fmaf(gw[k].x, P2.x, -gw[k].y * P2.y))),
+                               fmaf(f[k].x, P1.y, fmaf(f[k].y, P1.x, fmaf(gw[k].x, P2.y, gw[k].y * P2.x))));
+        };
         if (act) {
-            const int qbase = sd.c - L / 2 + t;
-            const float bp1 = sd.bp1;
-            const bool odd = t & 1;
-            static_for<PPT>([&](auto kc) {
-                constexpr int K = decltype(kc)::value;
-                constexpr int KP = K ^ (L / (2 * TW));  // (t + 16K) ^ (L/2) == t + 16*KP
-                const float w = __int_as_float(__ldg(&ce[TW * K]).y);
-                const int q = (qbase + TW * KP) & (N - 1);
-                float2 a = cscale(spec0[q], w), b = cscale(spec1[q], w * bp1);
-                if (odd) b = make_float2(-b.x, -b.y);  // t = Omega_{L/2} g1
-                g1[0][K] = b;
-                g0[0][K] = mul_jpow_rt(csub(a, b), t);  // f = Omega_{-L/4}(g0 - t); b mod 4 == t mod 4
-            });
-        } else {
-#pragma unroll
-            for (int k = 0; k < PPT; ++k) g0[0][k] = g1[0][k] = zero2();
-        }
-        team_fft<L, TW, PPT, +1, 1, false>(g0, b1, stw, sts, t, act);
-#pragma unroll
-        for (int k = PPT / 2; k < PPT; ++k) g0[0][k] = zero2();  // S-hat: elements >= L/2
-        team_fft<L, TW, PPT, -1, 1, false>(g0, b1, stw, sts, t, act);
-        if (act) {
-            const float2 ph = __ldg(&P.tw[theta_exp<N>(sd.cmodN, sy.smodN)]);  // conj(theta_n)
-            const float a = sd.rx_s0 / (float)L, s = sd.rx_s0;
             if (P.grid_full) {
                 float2* o = orow + sd.full_off + t;
 #pragma unroll
-                for (int k = 0; k < PPT; ++k) {
-                    const float2 tj = mul_jpow_rt(g1[0][k], t);
-                    o[TW * k] = cmul(make_float2(fmaf(g0[0][k].x, a, tj.x * s), fmaf(g0[0][k].y, a, tj.y * s)), ph);
-                }
+                for (int k = 0; k < PPT; ++k) o[TW * k] = outv(k);
             } else {
                 float2* o = orow + sd.act_off;
                 int inv[PPT];  // all entry loads in flight before the first store
 #pragma unroll
                 for (int k = 0; k < PPT; ++k) inv[k] = (int)(short)(__ldg(&ce[TW * k]).x & 0xffff);
 #pragma unroll
-                for (int k = 0; k < PPT; ++k) {
-                    if (inv[k] >= 0) {
-                        const float2 tj = mul_jpow_rt(g1[0][k], t);
-                        o[inv[k]] = cmul(make_float2(fmaf(g0[0][k].x, a, tj.x * s), fmaf(g0[0][k].y, a, tj.y * s)), ph);
-                    }
-                }
+                for (int k = 0; k < PPT; ++k)
+                    if (inv[k] >= 0) o[inv[k]] = outv(k);
             }
         }
-        __syncwarp();
     }
+    if (FCW_RX_HYBRID && done < gcount)
+        rx_short_warp<N, L>(P, tm, sy, spec0, spec1, orow, scr, stw, gstart + done, gcount - done);
 }
 
-template <int N, int L>
+// MIRROR: the kernel keeps the wrap-around spectrum copy rx_short_half needs
+// (the uniform L = 256 specialisation); generic kernels use the warp path.
+template <int N, int L, bool MIRROR = false>
 FCW_DI void rx_short_one(const KParams& P, const Team& tm, const SymDev& sy, const float2* spec0,
                          const float2* spec1, float2* orow, float2* scr, const float2* stw, int gs, int gc) {
     if constexpr (L <= N) {
         if constexpr (L <= 32)
             rx_short_thread<N, L>(P, tm, sy, spec0, spec1, orow, gs, gc);
-        else if constexpr (L == 256) {
+        else if constexpr (L == 256 && MIRROR) {
             if (P.fused)
                 rx_short_half<N, L>(P, tm, sy, spec0, spec1, orow, scr, stw, gs, gc);
             else
@@ -619,7 +748,7 @@ template <int N, int LU>
 FCW_DI void rx_short_all(const KParams& P, const Team& tm, const SymDev& sy, const float2* spec0,
                          const float2* spec1, float2* orow, float2* scr, const float2* stw) {
     if constexpr (LU > 0) {
-        rx_short_one<N, LU>(P, tm, sy, spec0, spec1, orow, scr, stw, 0, P.M);
+        rx_short_one<N, LU, LU == 256>(P, tm, sy, spec0, spec1, orow, scr, stw, 0, P.M);
     } else {
         for (int g = 0; g < P.n_groups; ++g) {
             const int gs = P.grp_start[g], gc = P.grp_count[g];
@@ -726,7 +855,6 @@ template <int N>
 constexpr int long_twl() {
     return N >= 1024 ? 6 : 0;
 }
-constexpr int kLtwLen = 64 + 4096 / 64;
 template <int G>
 FCW_DI Smem smem_layout(const KParams& P, int g) {
     extern __shared__ float4 smem_raw[];
@@ -738,7 +866,7 @@ FCW_DI Smem smem_layout(const KParams& P, int g) {
     s.scr = rest + (threadIdx.x >> 5) * P.scratch_stride;
     s.stw = rest + kWarps * P.scratch_stride;
     s.ltw = s.stw + P.stab_len;
-    s.s_item = reinterpret_cast<int*>(s.ltw + kLtwLen) + g;
+    s.s_item = reinterpret_cast<int*>(s.ltw + kLtwLen + P.tw16_len) + g;
     return s;
 }
 
@@ -759,6 +887,11 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) tx_kernel(const KP
     for (int i = tid; i < P.stab_len; i += kThreads) S.stw[i] = __ldg(&P.tw[i * (N / P.stab_len)]);
     if constexpr (long_twl<N>() > 0)
         for (int i = tid; i < 64 + N / 64; i += kThreads) S.ltw[i] = __ldg(&P.tw[i < 64 ? i : 64 * (i - 64)]);
+    // tw16[sel][m][t] = W_256^(m (t + 64 sel)) for the half-warp FFT_256
+    for (int i = tid; i < P.tw16_len; i += kThreads) {
+        const int sel = i >> 8, m = (i >> 4) & 15, t = i & 15;
+        S.ltw[kLtwLen + i] = __ldg(&P.tw[((m * (t + 64 * sel)) & 255) * (N / 256)]);
+    }
     __syncthreads();
 
     RunSource<G, DYN> runs(P, g);
@@ -851,6 +984,11 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) rx_kernel(const KP
     for (int i = tid; i < P.stab_len; i += kThreads) S.stw[i] = __ldg(&P.tw[i * (N / P.stab_len)]);
     if constexpr (long_twl<N>() > 0)
         for (int i = tid; i < 64 + N / 64; i += kThreads) S.ltw[i] = __ldg(&P.tw[i < 64 ? i : 64 * (i - 64)]);
+    // tw16[sel][m][t] = W_256^(m (t + 64 sel)) for the half-warp FFT_256
+    for (int i = tid; i < P.tw16_len; i += kThreads) {
+        const int sel = i >> 8, m = (i >> 4) & 15, t = i & 15;
+        S.ltw[kLtwLen + i] = __ldg(&P.tw[((m * (t + 64 * sel)) & 255) * (N / 256)]);
+    }
     __syncthreads();
 
     RunSource<G, DYN> runs(P, g);
@@ -887,6 +1025,13 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) rx_kernel(const KP
                 for (int m = 0; m < kPPT; ++m) {
                     spec0[gtid + T * m] = v[0][m];
                     spec1[gtid + T * m] = v[1][m];
+                    if constexpr (LU == 256) {
+                        // wrap-around copy of bins [0, L) at [N, N + L) (rx_short_half)
+                        if (T * m < LU && gtid + T * m < LU) {
+                            spec0[N + gtid + T * m] = v[0][m];
+                            spec1[N + gtid + T * m] = v[1][m];
+                        }
+                    }
                 }
             }
             team_sync<G>(g, TT);

@@ -99,7 +99,30 @@ __host__ __device__ constexpr int cx_brev(int v, int bits) {
 }
 
 // ----------------------------------------------------- register radix-2 DIT
-template <int L, int SIGN, int LEN, int K>
+// ZM: compile-time mask of positions (in the bit-reversed working order) that
+// are known to be zero at the start of stage LEN; butterflies with a known-zero
+// operand are reduced to copies / a single product (pruned transforms).
+__host__ __device__ constexpr unsigned long long zm_next(unsigned long long zm, int L, int LEN) {
+    unsigned long long out = 0;
+    const int H = LEN / 2;
+    for (int s = 0; s < L; s += LEN)
+        for (int k = 0; k < H; ++k) {
+            const bool z = ((zm >> (s + k)) & 1ull) && ((zm >> (s + k + H)) & 1ull);
+            if (z) out |= (1ull << (s + k)) | (1ull << (s + k + H));
+        }
+    return out;
+}
+__host__ __device__ constexpr unsigned long long zm_brev(unsigned long long zm, int L, int bits) {
+    unsigned long long out = 0;
+    for (int p = 0; p < L; ++p) {
+        int r = 0;
+        for (int i = 0; i < bits; ++i) r |= ((p >> i) & 1) << (bits - 1 - i);
+        if ((zm >> r) & 1ull) out |= 1ull << p;
+    }
+    return out;
+}
+
+template <int L, int SIGN, int LEN, int K, unsigned long long ZM = 0>
 FCW_DI void fft_stage(float2 (&x)[L]) {
     if constexpr (LEN <= L) {
         if constexpr (K < LEN / 2) {
@@ -108,7 +131,18 @@ FCW_DI void fft_stage(float2 (&x)[L]) {
             for (int s = 0; s < L; s += LEN) {
                 const float2 a = x[s + K];
                 const float2 b = x[s + K + H];
-                if constexpr (K == 0 || 4 * K == LEN) {
+                const bool za = (ZM >> (s + K)) & 1ull, zb = (ZM >> (s + K + H)) & 1ull;
+                if (za && zb) {
+                    x[s + K] = make_float2(0.f, 0.f);  // never read the (unset) zero registers
+                    x[s + K + H] = make_float2(0.f, 0.f);
+                } else if (zb) {
+                    x[s + K + H] = a;  // a + w*0, a - w*0
+                } else if (za) {
+                    float2 wb = b;
+                    if constexpr (K != 0) wb = cmul(b, make_float2(Tw<LEN, K, SIGN>::re, Tw<LEN, K, SIGN>::im));
+                    x[s + K] = wb;
+                    x[s + K + H] = make_float2(-wb.x, -wb.y);  // negation folds into consumers
+                } else if constexpr (K == 0 || 4 * K == LEN) {
                     // trivial twiddles 1 and -+j: 4 FADD
                     const float2 wb = (K == 0) ? b : (SIGN < 0 ? make_float2(b.y, -b.x) : make_float2(-b.y, b.x));
                     x[s + K] = cadd(a, wb);
@@ -134,14 +168,15 @@ FCW_DI void fft_stage(float2 (&x)[L]) {
                     x[s + K + H] = make_float2(fmaf(2.f, a.x, -y0r), fmaf(2.f, a.y, -y0i));
                 }
             }
-            fft_stage<L, SIGN, LEN, K + 1>(x);
+            fft_stage<L, SIGN, LEN, K + 1, ZM>(x);
         } else {
-            fft_stage<L, SIGN, LEN * 2, 0>(x);
+            fft_stage<L, SIGN, LEN * 2, 0, zm_next(ZM, L, LEN)>(x);
         }
     }
 }
 
-template <int L, int SIGN>
+// ZIN: compile-time mask of inputs (natural order) known to be zero.
+template <int L, int SIGN, unsigned long long ZIN = 0>
 FCW_DI void fft_reg(float2 (&x)[L]) {
     if constexpr (L == 1) return;
     constexpr int LB = cx_log2(L);
@@ -154,7 +189,7 @@ FCW_DI void fft_reg(float2 (&x)[L]) {
             x[j] = t;
         }
     }
-    fft_stage<L, SIGN, 2, 0>(x);
+    fft_stage<L, SIGN, 2, 0, zm_brev(ZIN, L, LB)>(x);
 }
 
 // ------------------------------------------------------------ team barriers
@@ -302,6 +337,65 @@ FCW_DI void team_fft(float2 (&v)[NF][PPT], float2* const* buf, const float2* __r
     } else {
         team_pass<n, T, PPT, SIGN, NF, CTA, 1, TWL>(v, buf, tw, ts, t, act, bar_id, bar_n);
     }
+}
+
+// Half-warp FFT_256, radix 16 x 16 with ONE shared-memory exchange.  Lane t of
+// a 16-lane team holds v[m] = x[t + 16 m] and receives v[k] = X[t + 16 k].
+//  * ZIN: inputs v[m] known to be zero (pruned first pass; never read).
+//  * eoff: the pass-2 twiddle exponent of lane t is (t + eoff) mod 256.  A
+//    non-zero eoff transforms the input rotated by a per-lane factor:
+//    eoff = 64 gives the transform of e^{SIGN 2 pi i 64 t / 256} x[t + 16 m]
+//    (j^t for SIGN = +1) at no cost, since that factor is common to every
+//    pass-1 input of lane t and so commutes into its pass-2 twiddle.
+//  * buf: the team's exchange buffer, >= 271 float2 (17 t + k / t + 17 m:
+//    conflict-free, immediate offsets).  stw[e] = exp(-2 pi i e / 256).
+// Both halves of the warp must call it (it uses __syncwarp).
+// tw16 (optional): per-lane twiddle table, tw16[sel][m][t] = exp(-2 pi i m (t + 64 sel) / 256)
+// for sel = eoff / 64 in {0, 1}: 15 conflict-free loads instead of 4 loads
+// and 11 complex products.
+template <int SIGN, unsigned long long ZIN = 0>
+FCW_DI void fft256_half(float2 (&v)[16], float2* buf, const float2* stw, int t, int eoff,
+                        const float2* tw16 = nullptr) {
+    fft_reg<16, SIGN, ZIN>(v);
+    __syncwarp();  // the previous use of buf has been read by every lane
+    float2* wp = buf + 17 * t;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) wp[k] = v[k];
+    __syncwarp();
+    const float2* rp = buf + t;
+#pragma unroll
+    for (int m = 0; m < 16; ++m) v[m] = rp[17 * m];
+    if (tw16) {
+        const float2* tp = tw16 + (eoff >> 6) * 256 + t;
+#pragma unroll
+        for (int m = 1; m < 16; ++m) {
+            float2 w = tp[16 * m];
+            if constexpr (SIGN > 0) w.y = -w.y;
+            v[m] = cmul(v[m], w);
+        }
+        fft_reg<16, SIGN>(v);
+        return;
+    }
+    const int e0 = (t + eoff) & 255;
+    auto ld = [&](int e) {
+        float2 x = stw[e & 255];
+        if constexpr (SIGN > 0) x.y = -x.y;
+        return x;
+    };
+    float2 w[16];
+    w[1] = ld(e0);
+    w[2] = ld(2 * e0);
+    w[4] = ld(4 * e0);
+    w[8] = ld(8 * e0);
+    w[3] = cmul(w[1], w[2]);
+    w[5] = cmul(w[1], w[4]);
+    w[6] = cmul(w[2], w[4]);
+    w[7] = cmul(w[3], w[4]);
+#pragma unroll
+    for (int k = 9; k < 16; ++k) w[k] = cmul(w[k - 8], w[8]);
+#pragma unroll
+    for (int m = 1; m < 16; ++m) v[m] = cmul(v[m], w[m]);
+    fft_reg<16, SIGN>(v);
 }
 
 }  // namespace fcw

@@ -57,6 +57,7 @@ struct KParams {
     int scratch_stride;  // float2 per warp scratch
     int stab_len;        // entries of the SMEM short-transform twiddle table (plan Lmax)
     int stage_off;       // TX: offset of the cp.async grid staging buffer in a warp's scratch
+    int tw16_len;        // float2 entries of the half-warp FFT_256 twiddle table in SMEM (0 or 512)
     int row_len;
     int grid_full;
     int fused;

@@ -2,10 +2,10 @@
 #include "fcw_k_inst.cuh"
 
 namespace fcw {
-FCW_KERNELS_GENERIC(16)
-FCW_KERNELS_GENERIC(32)
-FCW_KERNELS_GENERIC(64)
-FCW_KERNELS_GENERIC(128)
-FCW_KERNELS_GENERIC(256)
-FCW_KERNELS_GENERIC(512)
+FCW_KERNELS_NL(16, 0)
+FCW_KERNELS_NL(32, 0)
+FCW_KERNELS_NL(64, 0)
+FCW_KERNELS_NL(128, 0)
+FCW_KERNELS_NL(256, 0)
+FCW_KERNELS_NL(512, 0)
 }  // namespace fcw

@@ -10,30 +10,69 @@
 
 namespace fcw {
 
-KernelPair kernels_n16(int);
-KernelPair kernels_n32(int);
-KernelPair kernels_n64(int);
-KernelPair kernels_n128(int);
-KernelPair kernels_n256(int);
-KernelPair kernels_n512(int);
-KernelPair kernels_n1024(int);
-KernelPair kernels_n2048(int);
-KernelPair kernels_n4096(int);
+KernelPair kernels_n16_l0();
+KernelPair kernels_n32_l0();
+KernelPair kernels_n64_l0();
+KernelPair kernels_n128_l0();
+KernelPair kernels_n256_l0();
+KernelPair kernels_n512_l0();
+KernelPair kernels_n1024_l0();
+KernelPair kernels_n2048_l0();
+KernelPair kernels_n4096_l0();
+KernelPair kernels_n1024_l16();
+KernelPair kernels_n1024_l32();
+KernelPair kernels_n1024_l64();
+KernelPair kernels_n1024_l128();
+KernelPair kernels_n1024_l256();
+KernelPair kernels_n1024_l512();
+KernelPair kernels_n1024_l1024();
+KernelPair kernels_n2048_l16();
+KernelPair kernels_n2048_l32();
+KernelPair kernels_n2048_l64();
+KernelPair kernels_n2048_l128();
+KernelPair kernels_n2048_l256();
+KernelPair kernels_n2048_l512();
+KernelPair kernels_n2048_l1024();
+KernelPair kernels_n4096_l16();
+KernelPair kernels_n4096_l32();
+KernelPair kernels_n4096_l64();
+KernelPair kernels_n4096_l128();
+KernelPair kernels_n4096_l256();
+KernelPair kernels_n4096_l512();
+KernelPair kernels_n4096_l1024();
 
 namespace {
 
+KernelPair pick_l(int N, int LU) {
+#define FCW_PICK_L(NN)                         \
+    switch (LU) {                              \
+        case 16: return kernels_n##NN##_l16();   \
+        case 32: return kernels_n##NN##_l32();   \
+        case 64: return kernels_n##NN##_l64();   \
+        case 128: return kernels_n##NN##_l128(); \
+        case 256: return kernels_n##NN##_l256(); \
+        case 512: return kernels_n##NN##_l512(); \
+        case 1024: return kernels_n##NN##_l1024(); \
+        default: return kernels_n##NN##_l0();    \
+    }
+    switch (N) {
+        case 1024: FCW_PICK_L(1024)
+        case 2048: FCW_PICK_L(2048)
+        case 4096: FCW_PICK_L(4096)
+        default: return KernelPair{nullptr, nullptr, nullptr, nullptr};
+    }
+#undef FCW_PICK_L
+}
+
 KernelPair pick(int N, int LU) {
     switch (N) {
-        case 16: return kernels_n16(LU);
-        case 32: return kernels_n32(LU);
-        case 64: return kernels_n64(LU);
-        case 128: return kernels_n128(LU);
-        case 256: return kernels_n256(LU);
-        case 512: return kernels_n512(LU);
-        case 1024: return kernels_n1024(LU);
-        case 2048: return kernels_n2048(LU);
-        case 4096: return kernels_n4096(LU);
-        default: return KernelPair{nullptr, nullptr, nullptr, nullptr};
+        case 16: return kernels_n16_l0();
+        case 32: return kernels_n32_l0();
+        case 64: return kernels_n64_l0();
+        case 128: return kernels_n128_l0();
+        case 256: return kernels_n256_l0();
+        case 512: return kernels_n512_l0();
+        default: return pick_l(N, LU);
     }
 }
 
@@ -44,8 +83,13 @@ int uniform_L(const Plan& p) {
     return (L >= 16 && L <= 1024) ? L : 0;
 }
 
-int spec_stride(const Plan& p) {
-    const int ext = p.n_ext > p.N / 16 ? p.n_ext : p.N / 16;
+// RX with the half-warp L = 256 path keeps a wrap-around copy of bins [0, L)
+// at [N, N + L) (rx_kernel, rx_short_half).
+bool rx_mirror(const Plan& p) { return uniform_L(p) == 256; }
+
+int spec_stride(const Plan& p, bool mirror = false) {
+    int ext = p.n_ext > p.N / 16 ? p.n_ext : p.N / 16;
+    if (mirror && ext < p.Lmax) ext = p.Lmax;
     return (p.N + ext + 2 + 1) & ~1;
 }
 
@@ -65,15 +109,17 @@ int scratch_stride(const Plan& p, int LU, bool tx, bool rx_direct) {
 }
 
 int stab_len(const Plan& p) { return p.Lmax >= 64 ? p.Lmax : 0; }
+// per-lane twiddles of the half-warp FFT_256 (uniform L = 256 kernels)
+int tw16_len(const Plan& p) { return uniform_L(p) == 256 ? 512 : 0; }
 
 // Independent teams per CTA (must match teams_per_cta<N> in fcw_device.cuh).
 int teams(const Plan& p) { return (p.N >= 512 && p.N <= 4096) ? 4096 / p.N : 1; }
 
 size_t smem_bytes(const Plan& p, bool tx, bool rx_direct) {
     const int LU = uniform_L(p);
-    const size_t f2 = 2 * (size_t)teams(p) * spec_stride(p) +
+    const size_t f2 = 2 * (size_t)teams(p) * spec_stride(p, !tx && rx_mirror(p)) +
                       (size_t)kWarps * scratch_stride(p, LU, tx, rx_direct) + stab_len(p) +
-                      128 /* two-level long twiddles */ + (teams(p) + 1) / 2 /* run-id slots */;
+                      128 /* two-level long twiddles */ + tw16_len(p) + (teams(p) + 1) / 2 /* run-id slots */;
     return f2 * sizeof(float2);
 }
 
@@ -188,6 +234,7 @@ void fill_common(const Plan& p, KParams& kp) {
     kp.zero_list = p.d_zero;
     kp.tw = p.d_tw;
     kp.stab_len = stab_len(p);
+    kp.tw16_len = tw16_len(p);
     kp.stage_off = p.Lmax >= 64 ? scratch_one(p) : 0;
     const char* dbg = std::getenv("FCW_DEBUG_SKIP");
     kp.dbg_skip = dbg ? std::atoi(dbg) : 0;
@@ -199,6 +246,7 @@ size_t rx_smem_bytes(const Plan& p) { return smem_bytes(p, false, true); }
 cudaError_t launch_tx(const Plan& p, KParams& kp, int S, cudaStream_t st) {
     const int LU = uniform_L(p);
     kp.scratch_stride = scratch_stride(p, LU, true, false);
+    kp.spec_stride = spec_stride(p);
     kp.n_units = S;
     kp.teams = teams(p);
     kp.n_items = S * kp.nchunks;
@@ -210,6 +258,7 @@ cudaError_t launch_rx(const Plan& p, KParams& kp, int S, cudaStream_t st) {
     const int LU = uniform_L(p);
     const bool direct = !kp.fused;
     kp.scratch_stride = scratch_stride(p, LU, false, direct);
+    kp.spec_stride = spec_stride(p, rx_mirror(p));
     kp.n_units = S;
     kp.teams = teams(p);
     kp.n_items = S * kp.nchunks;
