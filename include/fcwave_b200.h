@@ -139,6 +139,33 @@ int fcw_rx(const fcw_plan* plan, const void* wave, int64_t wave_unit_stride, int
 int fcw_gen_qam(const fcw_plan* plan, uint64_t seed, int64_t unit0, int S, int bits_per_symbol,
                 void* grid, void* stream);
 
+/* --------------------------------------- link step around the path (f1, f3) */
+
+/* Per-unit link statistics of a received packed grid [S][B][row_active]
+ * against the seeded transmit grid of fcw_gen_qam(seed, unit0, bits): the EVM
+ * sums sum|y - x|^2, sum|x|^2 (evm_db, metrics.cpp:115-127) and the bit errors
+ * of the hard decisions (qam_demap ofdm.cpp:67-78, ber metrics.cpp:105-113),
+ * as accumulated per drop in run_scenario (scenario.cpp:469-494).  Decisions
+ * are computed in double exactly like the reference; sums are reduced in a
+ * fixed order (deterministic).  Blocking: stats go to host memory. */
+typedef struct fcw_link_stat {
+    double evm_num, evm_den;
+    int64_t bit_errors, n_bits;
+} fcw_link_stat;
+int fcw_link_stats(const fcw_plan* plan, const void* grid, int64_t grid_unit_stride, int S, uint64_t seed,
+                   int64_t unit0, int bits_per_symbol, fcw_link_stat* stats, void* stream);
+
+/* awgn_with_variance (channel.cpp:136-141) on S device waveforms in place:
+ * unit u draws GaussianRng(derive_seed(seed, unit0 + u)) (channel.cpp:37-48),
+ * two draws per sample; v += sqrt(sigma2) * n in double, stored as fp32. */
+int fcw_awgn(const fcw_plan* plan, void* wave, int64_t wave_unit_stride, int64_t wave_len, int S, double sigma2,
+             uint64_t seed, int64_t unit0, void* stream);
+
+/* measure_power (channel.cpp:148-155) per unit: mean |v|^2 over
+ * [begin, end) clipped to [0, wave_len).  Blocking: power[S] on the host. */
+int fcw_wave_power(const fcw_plan* plan, const void* wave, int64_t wave_unit_stride, int64_t wave_len, int S,
+                   int64_t begin, int64_t end, double* power, void* stream);
+
 /* -------------------------------------------------- host-buffer entry points */
 
 /* Same as fcw_tx / fcw_rx with HOST buffers (pinned via fcw_host_alloc for

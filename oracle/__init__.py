@@ -103,6 +103,15 @@ def lib():
         L.fco_qam_map.restype = None
         L.fco_gen_grid.argtypes = [C.c_uint64, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int, _f64p]
         L.fco_gen_grid.restype = None
+        L.fco_qam_demap.argtypes = [C.c_int, C.c_double, C.c_double]
+        L.fco_qam_demap.restype = C.c_uint
+        _i64p = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
+        L.fco_link_stats.argtypes = [_f64p, C.c_uint64, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int, _f64p, _i64p]
+        L.fco_link_stats.restype = None
+        L.fco_awgn.argtypes = [_f64p, C.c_int64, C.c_double, C.c_uint64]
+        L.fco_awgn.restype = None
+        L.fco_measure_power.argtypes = [_f64p, C.c_int64, C.c_int64, C.c_int64]
+        L.fco_measure_power.restype = C.c_double
     return _lib
 
 
@@ -132,6 +141,16 @@ def ref():
         R.fcwref_bench_txrx.argtypes = [C.c_int, C.c_double, _i32p, C.c_int, C.c_int, _i32p, _i32p, _f64p,
                                         _i32p, _i32p, _f32p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]
         R.fcwref_bench_txrx.restype = C.c_double
+        _u32p = np.ctypeslib.ndpointer(dtype=np.uint32, flags="C_CONTIGUOUS")
+        _u8p = np.ctypeslib.ndpointer(dtype=np.uint8, flags="C_CONTIGUOUS")
+        R.fcwref_qam_demap.argtypes = [C.c_int, _f64p, C.c_int, _u32p]
+        R.fcwref_qam_map.argtypes = [C.c_int, _u32p, C.c_int, _f64p]
+        R.fcwref_ber.argtypes = [_u8p, _u8p, C.c_longlong, C.POINTER(C.c_double)]
+        R.fcwref_evm_db.argtypes = [_f64p, _f64p, C.c_longlong, C.POINTER(C.c_double)]
+        R.fcwref_awgn_with_variance.argtypes = [_f64p, C.c_longlong, C.c_double, C.c_ulonglong]
+        R.fcwref_measure_power.argtypes = [_f64p, C.c_longlong, C.c_longlong, C.c_longlong, C.POINTER(C.c_double)]
+        R.fcwref_awgn_noise_variance.argtypes = [_f64p, C.c_longlong, C.c_double, C.c_int, C.c_int,
+                                                 C.POINTER(C.c_double)]
     return _ref
 
 
@@ -328,6 +347,47 @@ def gen_grid(seed: int, unit0: int, units: int, B: int, A: int, bits_per_symbol:
     return out.view(np.complex128).reshape(units, B, A)
 
 
+# ------------------------------------------------------- link step (f1/f3)
+def qam_demap(bits_per_symbol: int, y) -> np.ndarray:
+    """ofdm.cpp:67-78 hard decision, per element (256-QAM extended)."""
+    y = np.asarray(y, np.complex128).reshape(-1)
+    L = lib()
+    return np.array([L.fco_qam_demap(bits_per_symbol, float(v.real), float(v.imag)) for v in y], np.uint32)
+
+
+def link_stats(rx, seed: int, unit0: int, bits_per_symbol: int):
+    """Per-unit (evm_num, evm_den, bit_errors) of a packed rx grid [units][B][A]
+    against the seeded transmit grid (scenario.cpp:469-494, metrics.cpp:105-127)."""
+    rx = np.ascontiguousarray(rx, np.complex128)
+    units, B, A = rx.shape
+    out = np.zeros(2 * units, np.float64)
+    errs = np.zeros(units, np.int64)
+    lib().fco_link_stats(rx.view(np.float64).reshape(-1), seed, unit0, units, B, A, bits_per_symbol, out, errs)
+    return out[0::2].copy(), out[1::2].copy(), errs
+
+
+def awgn(wave, sigma2: float, seed: int) -> np.ndarray:
+    """channel.cpp:136-141 awgn_with_variance (returns a new array)."""
+    w = _c128(wave).copy()
+    lib().fco_awgn(w.view(np.float64), len(w), sigma2, seed)
+    return w
+
+
+def measure_power(wave, begin: int, end: int) -> float:
+    """channel.cpp:148-155."""
+    w = _c128(wave)
+    return float(lib().fco_measure_power(w.view(np.float64), len(w), begin, end))
+
+
+def evm_db(num: float, den: float) -> float:
+    """metrics.cpp:115-127 from the accumulated sums."""
+    if den <= 0.0:
+        raise ValueError("zero reference power")
+    if num <= 0.0:
+        return 300.0
+    return min(300.0, -10.0 * float(np.log10(num / den)))
+
+
 # ------------------------------------------------------- compiled reference
 class Ref:
     """Thin wrappers over oracle/_ref/libfcwave_ref.so (the real reference)."""
@@ -386,3 +446,55 @@ class Ref:
         if t < 0:
             raise OracleError(R.fcwref_last_error().decode())
         return t, chk.value
+
+    # ---- link step (f1/f3) through the reference's own functions
+    @staticmethod
+    def qam_demap(bits_per_symbol: int, y) -> np.ndarray:
+        y = _c128(np.asarray(y).reshape(-1))
+        out = np.zeros(len(y), np.uint32)
+        _check(ref().fcwref_qam_demap(bits_per_symbol, y.view(np.float64), len(y), out), "ref qam_demap", ref())
+        return out
+
+    @staticmethod
+    def qam_map(bits_per_symbol: int, syms) -> np.ndarray:
+        s = np.ascontiguousarray(syms, np.uint32)
+        out = np.zeros(2 * len(s), np.float64)
+        _check(ref().fcwref_qam_map(bits_per_symbol, s, len(s), out), "ref qam_map", ref())
+        return out.view(np.complex128)
+
+    @staticmethod
+    def ber(a, b) -> float:
+        a = np.ascontiguousarray(a, np.uint8)
+        b = np.ascontiguousarray(b, np.uint8)
+        v = C.c_double()
+        _check(ref().fcwref_ber(a, b, len(a), C.byref(v)), "ref ber", ref())
+        return v.value
+
+    @staticmethod
+    def evm_db(ref_grid, rx) -> float:
+        r = _c128(np.asarray(ref_grid).reshape(-1))
+        x = _c128(np.asarray(rx).reshape(-1))
+        v = C.c_double()
+        _check(ref().fcwref_evm_db(r.view(np.float64), x.view(np.float64), len(r), C.byref(v)), "ref evm_db", ref())
+        return v.value
+
+    @staticmethod
+    def awgn_with_variance(wave, sigma2: float, seed: int) -> np.ndarray:
+        w = _c128(wave).copy()
+        _check(ref().fcwref_awgn_with_variance(w.view(np.float64), len(w), sigma2, seed), "ref awgn", ref())
+        return w
+
+    @staticmethod
+    def measure_power(wave, begin: int, end: int) -> float:
+        w = _c128(wave)
+        v = C.c_double()
+        _check(ref().fcwref_measure_power(w.view(np.float64), len(w), begin, end, C.byref(v)), "ref power", ref())
+        return v.value
+
+    @staticmethod
+    def awgn_noise_variance(wave, snr_db: float, n_fft: int, n_active: int) -> float:
+        w = _c128(wave)
+        v = C.c_double()
+        _check(ref().fcwref_awgn_noise_variance(w.view(np.float64), len(w), snr_db, n_fft, n_active, C.byref(v)),
+               "ref noise variance", ref())
+        return v.value

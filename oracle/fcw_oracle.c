@@ -489,3 +489,94 @@ void fco_gen_grid(uint64_t seed, int64_t unit0, int units, int B, int A, int bit
         }
     }
 }
+
+/* ------------------------------------------------------------ link step (f1)
+ * The step on either side of the path in the reference's link simulation
+ * (scenario.cpp:469-494): hard-decision demap, bit errors and EVM sums.   */
+
+/* ofdm.cpp:67-78 (qam_demap): per-axis slice with lround, clamp, Gray encode;
+ * extended to k=4 (256-QAM) with the same formulas. */
+unsigned fco_qam_demap(int bits_per_symbol, double re, double im) {
+    const int k = bits_per_symbol / 2;
+    const int levels = 1 << k;
+    const double s = 1.0 / sqrt(2.0 * ((double)levels * levels - 1.0) / 3.0);
+    unsigned out[2];
+    const double v[2] = {re, im};
+    for (int a = 0; a < 2; ++a) {
+        /* static_cast<int>(std::lround(...)) as in the reference: the long
+         * result is narrowed to int (modular) before the clamp */
+        int idx = (int)lround((v[a] / s - 1.0 + levels) / 2.0);
+        if (idx < 0) idx = 0;
+        if (idx >= levels) idx = levels - 1;
+        out[a] = (unsigned)idx ^ ((unsigned)idx >> 1);
+    }
+    return out[0] | (out[1] << k);
+}
+
+/* Per-unit link statistics of a received packed grid against the seeded
+ * transmit grid of fco_gen_grid: EVM numerator/denominator sums
+ * (metrics.cpp:115-127 evm_db, scenario.cpp:481-484) and bit errors of the
+ * hard decisions (metrics.cpp:105-113 ber, scenario.cpp:486-491).  The
+ * transmitted bits are re-drawn from the same splitmix64 streams.
+ * out: per unit {evm_num, evm_den}; errs: per unit bit errors.  The sums run
+ * in element order. */
+void fco_link_stats(const double* rx, uint64_t seed, int64_t unit0, int units, int B, int A,
+                    int bits_per_symbol, double* out, int64_t* errs) {
+    for (int u = 0; u < units; ++u) {
+        uint64_t st = fco_derive_seed(seed, (uint64_t)(unit0 + u));
+        if (st == 0) st = 0x1234567890abcdefULL;
+        const double* y = rx + 2 * (size_t)u * B * A;
+        double num = 0.0, den = 0.0;
+        int64_t e = 0;
+        for (int64_t i = 0; i < (int64_t)B * A; ++i) {
+            unsigned sym = 0;
+            for (int b = 0; b < bits_per_symbol; ++b) sym |= (unsigned)(fco_splitmix64(&st) & 1u) << b;
+            double xr, xi;
+            fco_qam_map(bits_per_symbol, sym, &xr, &xi);
+            const double dr = y[2 * i] - xr, di = y[2 * i + 1] - xi;
+            num += dr * dr + di * di;
+            den += xr * xr + xi * xi;
+            const unsigned got = fco_qam_demap(bits_per_symbol, y[2 * i], y[2 * i + 1]);
+            unsigned diff = got ^ sym;
+            for (int b = 0; b < bits_per_symbol; ++b) e += (diff >> b) & 1u;
+        }
+        out[2 * u] = num;
+        out[2 * u + 1] = den;
+        errs[u] = e;
+    }
+}
+
+/* channel.cpp:37-42 (GaussianRng::next_complex): two draws, Box-Muller with
+ * variance 1/2 per axis. */
+void fco_gauss_complex(uint64_t* state, double* re, double* im) {
+    const double u1 = ((double)(fco_splitmix64(state) >> 11) + 1.0) * 0x1p-53;
+    const double u2 = (double)(fco_splitmix64(state) >> 11) * 0x1p-53;
+    const double r = sqrt(-log(u1));
+    const double pi = 3.14159265358979323846;
+    *re = r * cos(2.0 * pi * u2);
+    *im = r * sin(2.0 * pi * u2);
+}
+
+/* channel.cpp:136-141 (awgn_with_variance): v += sqrt(sigma2) * n, one
+ * GaussianRng(seed) stream over the samples in order. */
+void fco_awgn(double* wave, int64_t len, double sigma2, uint64_t seed) {
+    uint64_t st = seed ? seed : 0x1234567890abcdefULL;
+    const double s = sqrt(sigma2);
+    for (int64_t t = 0; t < len; ++t) {
+        double nr, ni;
+        fco_gauss_complex(&st, &nr, &ni);
+        wave[2 * t] += s * nr;
+        wave[2 * t + 1] += s * ni;
+    }
+}
+
+/* channel.cpp:148-155 (measure_power): mean |v|^2 over [begin, end) clipped
+ * to the waveform; -1 for an empty span (the reference throws). */
+double fco_measure_power(const double* wave, int64_t len, int64_t begin, int64_t end) {
+    if (begin < 0) begin = 0;
+    if (end > len) end = len;
+    if (end <= begin) return -1.0;
+    double p = 0.0;
+    for (int64_t t = begin; t < end; ++t) p += wave[2 * t] * wave[2 * t] + wave[2 * t + 1] * wave[2 * t + 1];
+    return p / (double)(end - begin);
+}

@@ -75,6 +75,15 @@ void fco_qam_map(int bits_per_symbol, unsigned symbol_bits, double* re, double* 
 void fco_gen_grid(uint64_t seed, int64_t unit0, int units, int B, int A, int bits_per_symbol,
                   double* packed);
 
+/* Link step around the path (f1/f3): ofdm.cpp:67-78, metrics.cpp:105-127,
+ * scenario.cpp:469-494, channel.cpp:37-42,136-155. */
+unsigned fco_qam_demap(int bits_per_symbol, double re, double im);
+void fco_link_stats(const double* rx, uint64_t seed, int64_t unit0, int units, int B, int A,
+                    int bits_per_symbol, double* out, int64_t* errs);
+void fco_gauss_complex(uint64_t* state, double* re, double* im);
+void fco_awgn(double* wave, int64_t len, double sigma2, uint64_t seed);
+double fco_measure_power(const double* wave, int64_t len, int64_t begin, int64_t end);
+
 #ifdef __cplusplus
 }
 #endif

@@ -13,7 +13,9 @@
  * exceptions map to status codes: invalid_argument -> 1, out_of_range -> 2,
  * anything else -> 3; the message is kept in fcwref_last_error().
  */
+#include "fcwave/channel.hpp"
 #include "fcwave/fc_core.hpp"
+#include "fcwave/metrics.hpp"
 #include "fcwave/fc_sync.hpp"
 #include "fcwave/numerology.hpp"
 #include "fcwave/ofdm.hpp"
@@ -247,6 +249,66 @@ double fcwref_bench_txrx(int N, double overlap, const int* cp, int B, int M, con
         if (checksum) *checksum = total;
     });
     return rc == 0 ? elapsed : -1.0;
+}
+
+
+/* ---- link step (f1/f3): the reference's own demap / metrics / channel ---- */
+int fcwref_qam_demap(int bits_per_symbol, const double* y, int n, unsigned* out) {
+    return guarded([&] {
+        const fcwave::Modulation m = bits_per_symbol == 2   ? fcwave::Modulation::QPSK
+                                     : bits_per_symbol == 4 ? fcwave::Modulation::QAM16
+                                                            : fcwave::Modulation::QAM64;
+        for (int i = 0; i < n; ++i) out[i] = fcwave::qam_demap(m, cd{y[2 * i], y[2 * i + 1]});
+    });
+}
+
+int fcwref_qam_map(int bits_per_symbol, const unsigned* sym, int n, double* out) {
+    return guarded([&] {
+        const fcwave::Modulation m = bits_per_symbol == 2   ? fcwave::Modulation::QPSK
+                                     : bits_per_symbol == 4 ? fcwave::Modulation::QAM16
+                                                            : fcwave::Modulation::QAM64;
+        for (int i = 0; i < n; ++i) {
+            const cd v = fcwave::qam_map(m, sym[i]);
+            out[2 * i] = v.real();
+            out[2 * i + 1] = v.imag();
+        }
+    });
+}
+
+int fcwref_ber(const unsigned char* a, const unsigned char* b, long long n, double* out) {
+    return guarded([&] {
+        *out = fcwave::ber(std::vector<std::uint8_t>(a, a + n), std::vector<std::uint8_t>(b, b + n));
+    });
+}
+
+int fcwref_evm_db(const double* ref, const double* rx, long long n, double* out) {
+    return guarded([&] { *out = fcwave::evm_db(to_cvec(ref, (std::size_t)n), to_cvec(rx, (std::size_t)n)); });
+}
+
+int fcwref_awgn_with_variance(double* wave, long long n, double sigma2, unsigned long long seed) {
+    return guarded([&] {
+        fcwave::Waveform w;
+        w.samples = to_cvec(wave, (std::size_t)n);
+        fcwave::awgn_with_variance(w, sigma2, seed);
+        from_cvec(w.samples, wave);
+    });
+}
+
+int fcwref_measure_power(const double* wave, long long n, long long begin, long long end, double* out) {
+    return guarded([&] {
+        fcwave::Waveform w;
+        w.samples = to_cvec(wave, (std::size_t)n);
+        *out = fcwave::measure_power(w, begin, end);
+    });
+}
+
+int fcwref_awgn_noise_variance(const double* wave, long long n, double snr_db, int n_fft, int n_active,
+                               double* out) {
+    return guarded([&] {
+        fcwave::Waveform w;
+        w.samples = to_cvec(wave, (std::size_t)n);
+        *out = fcwave::awgn_noise_variance(w, snr_db, n_fft, n_active);
+    });
 }
 
 }  // extern "C"

@@ -27,7 +27,12 @@ EXPORTS = [
     "fcw_tx_host", "fcw_rx_host", "fcw_host_alloc", "fcw_host_free", "fcw_derive_fc_params", "fcw_cp_schedule",
     "fcw_nr_cp_schedule", "fcw_cp_truncate", "fcw_first_block_overlap", "fcw_design_window",
     "fcw_centered_active_map", "fcw_symbol_sigma", "fcw_combined_length", "fcw_last_error", "fcw_version",
+    "fcw_link_stats", "fcw_awgn", "fcw_wave_power",
 ]
+
+
+class LinkStatC(C.Structure):
+    _fields_ = [("evm_num", C.c_double), ("evm_den", C.c_double), ("bit_errors", C.c_int64), ("n_bits", C.c_int64)]
 
 
 class FcParamsC(C.Structure):
@@ -89,6 +94,9 @@ def lib() -> C.CDLL:
     L.fcw_tx.argtypes = [vp, vp, i64, vp, i64, C.c_int, C.c_uint, vp]
     L.fcw_rx.argtypes = [vp, vp, i64, i64, i64, vp, i64, C.c_int, C.c_uint, vp]
     L.fcw_gen_qam.argtypes = [vp, C.c_uint64, i64, C.c_int, C.c_int, vp, vp]
+    L.fcw_link_stats.argtypes = [vp, vp, i64, C.c_int, C.c_uint64, i64, C.c_int, C.POINTER(LinkStatC), vp]
+    L.fcw_awgn.argtypes = [vp, vp, i64, i64, C.c_int, C.c_double, C.c_uint64, i64, vp]
+    L.fcw_wave_power.argtypes = [vp, vp, i64, i64, C.c_int, i64, i64, C.POINTER(C.c_double), vp]
     L.fcw_tx_host.argtypes = [vp, vp, vp, C.c_int, C.c_uint]
     L.fcw_rx_host.argtypes = [vp, vp, i64, i64, vp, C.c_int, C.c_uint]
     L.fcw_host_alloc.argtypes = [C.c_size_t]

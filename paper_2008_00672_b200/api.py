@@ -10,6 +10,7 @@ S independent (antenna stream x frame) units per call.
 from __future__ import annotations
 
 import ctypes as C
+import math
 from dataclasses import dataclass, field
 from typing import Sequence
 
@@ -292,6 +293,32 @@ class Plan:
         check(lib().fcw_gen_qam(self._h, seed, unit0, S, bits_per_symbol, _dev_ptr(grid), _stream_ptr(stream)))
 
     # -- host entry points (numpy complex64, C-contiguous)
+    # ---- link step around the path
+    def link_stats(self, grid, S: int, seed: int, unit0: int, bits_per_symbol: int, stream=None,
+                   grid_stride: int = 0) -> "LinkStats":
+        """Per-unit EVM sums and hard-decision bit errors of a received packed
+        device grid against the seeded transmit grid (scenario.cpp:469-494)."""
+        out = (_lib.LinkStatC * max(S, 1))()
+        check(lib().fcw_link_stats(self._h, _dev_ptr(grid), grid_stride, S, seed, unit0, bits_per_symbol, out,
+                                   _stream_ptr(stream)))
+        return LinkStats(np.array([o.evm_num for o in out[:S]]), np.array([o.evm_den for o in out[:S]]),
+                         np.array([o.bit_errors for o in out[:S]], np.int64),
+                         np.array([o.n_bits for o in out[:S]], np.int64))
+
+    def awgn(self, wave, wave_len: int, S: int, sigma2: float, seed: int, unit0: int = 0, stream=None,
+             wave_stride: int = 0) -> None:
+        """awgn_with_variance (channel.cpp:136-141) in place on S device waveforms."""
+        check(lib().fcw_awgn(self._h, _dev_ptr(wave), wave_stride, wave_len, S, sigma2, seed, unit0,
+                             _stream_ptr(stream)))
+
+    def wave_power(self, wave, wave_len: int, S: int, begin: int, end: int, stream=None,
+                   wave_stride: int = 0) -> np.ndarray:
+        """measure_power (channel.cpp:148-155) per unit."""
+        out = (C.c_double * max(S, 1))()
+        check(lib().fcw_wave_power(self._h, _dev_ptr(wave), wave_stride, wave_len, S, begin, end, out,
+                                   _stream_ptr(stream)))
+        return np.array(out[:S])
+
     def tx_host(self, grid: np.ndarray, S: int, full: bool = False, out: np.ndarray | None = None) -> np.ndarray:
         g = np.ascontiguousarray(grid, dtype=np.complex64)
         if g.size != S * self.B * self.row(full):
@@ -417,3 +444,36 @@ def rx_discontinuous(w: Waveform, cfg: SubbandConfig, cps: CpSchedule, N: int, o
                      simplified: bool = False) -> list[np.ndarray]:
     """fc_sync.hpp:78-80 — returns B columns of L complex values."""
     return list(rx_discontinuous_all(w, [cfg], cps, N, overlap, simplified)[0])
+
+
+# ------------------------------------------------------------ link metrics
+@dataclass
+class LinkStats:
+    """Per-unit sums of the link step (scenario.cpp:481-491)."""
+    evm_num: np.ndarray
+    evm_den: np.ndarray
+    bit_errors: np.ndarray
+    n_bits: np.ndarray
+
+    def evm_db(self) -> float:
+        return evm_db_from_sums(float(np.sum(self.evm_num)), float(np.sum(self.evm_den)))
+
+    def ber(self) -> float:
+        return float(np.sum(self.bit_errors)) / float(np.sum(self.n_bits))
+
+
+def evm_db_from_sums(num: float, den: float) -> float:
+    """metrics.cpp:115-127 (evm_db) from accumulated sums: -10 log10(num/den),
+    300 dB cap; zero reference power is an error."""
+    if den <= 0.0:
+        raise ValueError("zero reference power")
+    if num <= 0.0:
+        return 300.0
+    return min(300.0, -10.0 * math.log10(num / den))
+
+
+def awgn_noise_variance(power: float, snr_db: float, n_fft: int, n_active_total: int) -> float:
+    """channel.cpp:120-127: Es per active subcarrier over an n_fft demodulation
+    window divided by the linear SNR."""
+    es = power * n_fft / n_active_total
+    return es / 10.0 ** (snr_db / 10.0)

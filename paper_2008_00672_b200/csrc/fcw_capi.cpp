@@ -636,6 +636,56 @@ int fcw_gen_qam(const fcw_plan* p, uint64_t seed, int64_t unit0, int S, int bits
     return FCW_OK;
 }
 
+// ------------------------------------------------------------- link step
+
+int fcw_link_stats(const fcw_plan* p, const void* grid, int64_t grid_stride, int S, uint64_t seed, int64_t unit0,
+                   int bits, fcw_link_stat* stats, void* stream) {
+    if (!p || !grid || !stats) return fail(FCW_EINVAL, "null argument");
+    if (bits != 2 && bits != 4 && bits != 6 && bits != 8) return fail(FCW_EINVAL, "bits_per_symbol must be 2,4,6,8");
+    if (S < 0) return fail(FCW_EINVAL, "negative unit count");
+    if (S == 0) return FCW_OK;
+    const int64_t per_unit = (int64_t)p->B * p->row_active;
+    if (grid_stride == 0) grid_stride = per_unit;
+    if (grid_stride < per_unit) return fail(FCW_EINVAL, "grid unit stride too small");
+    std::vector<double> num(S), den(S);
+    std::vector<long long> err(S);
+    const cudaError_t e = fcw::link_stats(*p, static_cast<const float2*>(grid), grid_stride, S, seed, unit0, bits,
+                                          num.data(), den.data(), err.data(), static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "link_stats");
+    for (int u = 0; u < S; ++u) stats[u] = fcw_link_stat{num[u], den[u], err[u], per_unit * bits};
+    return FCW_OK;
+}
+
+int fcw_awgn(const fcw_plan* p, void* wave, int64_t wave_stride, int64_t wave_len, int S, double sigma2,
+             uint64_t seed, int64_t unit0, void* stream) {
+    if (!p || !wave) return fail(FCW_EINVAL, "null argument");
+    if (S < 0 || wave_len < 0) return fail(FCW_EINVAL, "negative size");
+    if (!(sigma2 >= 0.0)) return fail(FCW_EINVAL, "noise variance must be >= 0");
+    if (wave_stride == 0) wave_stride = wave_len;
+    if (wave_stride < wave_len) return fail(FCW_EINVAL, "waveform unit stride smaller than its length");
+    if (S == 0 || wave_len == 0) return FCW_OK;
+    const cudaError_t e = fcw::awgn(static_cast<float2*>(wave), wave_stride, wave_len, S, sigma2, seed, unit0,
+                                    static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "awgn launch");
+    return FCW_OK;
+}
+
+int fcw_wave_power(const fcw_plan* p, const void* wave, int64_t wave_stride, int64_t wave_len, int S, int64_t begin,
+                   int64_t end, double* power, void* stream) {
+    if (!p || !wave || !power) return fail(FCW_EINVAL, "null argument");
+    if (S < 0) return fail(FCW_EINVAL, "negative unit count");
+    if (wave_stride == 0) wave_stride = wave_len;
+    if (wave_stride < wave_len) return fail(FCW_EINVAL, "waveform unit stride smaller than its length");
+    begin = std::max<int64_t>(begin, 0);
+    end = std::min<int64_t>(end, wave_len);
+    if (end <= begin) return fail(FCW_EINVAL, "empty measurement span");  // channel.cpp:151
+    if (S == 0) return FCW_OK;
+    const cudaError_t e = fcw::wave_power(static_cast<const float2*>(wave), wave_stride, S, begin, end, power,
+                                          static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "wave_power");
+    return FCW_OK;
+}
+
 // ------------------------------------------------------ host-buffer pipeline
 
 namespace {

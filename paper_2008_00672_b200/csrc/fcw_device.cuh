@@ -113,6 +113,9 @@ constexpr int kTw16Len = 512;            // fft256_half per-lane twiddles (unifo
 #ifndef FCW_TX_DST1
 #define FCW_TX_DST1 0  // TX half-warp scatter: decode bin destinations once for both blocks
 #endif
+#ifndef FCW_TX_LS
+#define FCW_TX_LS 0  // TX half-warp: both block DFTs in lockstep
+#endif
 #ifndef FCW_TW16
 #define FCW_TW16 1
 #endif
@@ -422,6 +425,27 @@ FCW_DI void tx_short_half(const KParams& P, const Team& tm, const SymDev& sy, co
             });
         };
 #endif
+#if FCW_TX_LS
+        {
+            // block 0: e = t + 16 m in [L/4 - lcp, 3L/4) holds x[(e - L/4) mod L] = v[(m - 4) mod 16];
+            // block 1: e in [L/4, 3L/4) holds x[e + L/4] = v[m + 4]; both DFTs in lockstep
+            float2 u0[PPT], u1[PPT];
+#pragma unroll
+            for (int k = 0; k < PPT; ++k) {
+                if (k >= 4 && k < 12)
+                    u0[k] = v[k - 4];
+                else if (k < 4)
+                    u0[k] = (t + TW * k >= L / 4 - lcp) ? v[k + 12] : zero2();
+                else
+                    u0[k] = zero2();  // k >= 12: known zero (not read)
+                u1[k] = (k >= 4 && k < 12) ? v[k + 4] : zero2();
+            }
+            fft256_half2<-1, 0xF000ull, 0xF00Full>(u0, u1, buf, t, tw16_of(P, stw));
+            scatter(u0, spec0, 1.f);
+            scatter(u1, spec1, sd.bp1);
+        }
+    }
+#else
         {
             // block 0: e = t + 16 m in [L/4 - lcp, 3L/4) holds x[(e - L/4) mod L] = v[(m - 4) mod 16]
             float2 u[PPT];
@@ -446,6 +470,7 @@ FCW_DI void tx_short_half(const KParams& P, const Team& tm, const SymDev& sy, co
             scatter(u, spec1, sd.bp1);
         }
     }
+#endif
     if (done < gcount)
         tx_short_warp_lockstep<N, L>(P, tm, sy, row, spec0, spec1, scr, stw, gstart + done, gcount - done);
 }

@@ -136,6 +136,13 @@ cudaError_t launch_rx(const Plan& plan, KParams& kp, int S, cudaStream_t st);
 cudaError_t launch_gen_qam(const Plan& plan, uint64_t seed, long long unit0, int S, int bits,
                            float2* out, cudaStream_t st);
 size_t tx_smem_bytes(const Plan& plan);
+// fcw_link.cu (link step around the path; blocking where results go to the host)
+cudaError_t link_stats(const Plan& p, const float2* grid, long long stride, int S, uint64_t seed, long long unit0,
+                       int bits, double* evm_num, double* evm_den, long long* errors, cudaStream_t st);
+cudaError_t awgn(float2* wave, long long stride, long long len, int S, double sigma2, uint64_t seed,
+                 long long unit0, cudaStream_t st);
+cudaError_t wave_power(const float2* wave, long long stride, int S, long long begin, long long end, double* power,
+                       cudaStream_t st);
 size_t rx_smem_bytes(const Plan& plan);
 void fill_common(const Plan& plan, KParams& kp);
 
