@@ -166,6 +166,41 @@ int fcw_awgn(const fcw_plan* plan, void* wave, int64_t wave_unit_stride, int64_t
 int fcw_wave_power(const fcw_plan* plan, const void* wave, int64_t wave_unit_stride, int64_t wave_len, int S,
                    int64_t begin, int64_t end, double* power, void* stream);
 
+/* ------------------------------------ continuous FC filterbank (row f2) */
+
+/* Replaces tx_continuous / rx_continuous (fc_core.hpp:64-77, fc_core.cpp:
+ * 155-223): blocks hop L_S = L/2 (low rate) and N_S = N/2 (high rate).  The
+ * plan fixes N, overlap (0.5), the subbands (window, c, L; active_bins and
+ * n_active are ignored: every bin is carried), the TX low-rate stream length
+ * of each subband (CpOfdmSignal::samples.size()), the RX waveform length and
+ * the first subband's first low-rate CP length l_cp0 (for useful0,
+ * fc_core.cpp:192-196).  Internally a block pair (2n, 2n+1) is one cp = 0
+ * symbol of the fused kernels (see fcw_cont.cu). */
+typedef struct fcw_cont_plan fcw_cont_plan;
+typedef struct fcw_cont_info {
+    int N, M;
+    int64_t tx_len;       /* reference waveform length: max_m (R_tot,m - 1) N_S + N */
+    int64_t tx_stride;    /* samples per unit written by fcw_tx_continuous (>= tx_len; the tail is zero) */
+    int64_t useful0;      /* Waveform::useful0 = round(overlap N) + I_0 l_cp0 */
+    int64_t stream_total; /* sum_m stream_len[m]: TX input samples per unit */
+    int64_t rx_wave_len;  /* RX input samples per unit */
+    int64_t rx_out_total; /* sum_m R_tot,m L_S,m: RX output samples per unit */
+    int tx_pairs, rx_pairs; /* block pairs per unit */
+} fcw_cont_info;
+int fcw_cont_plan_create(fcw_cont_plan** plan, int N, double overlap, const fcw_subband* subbands, int M,
+                         const int64_t* stream_len, int64_t rx_wave_len, int l_cp0);
+void fcw_cont_plan_destroy(fcw_cont_plan* plan);
+/* rx_out_len / rx_out_off (M entries each, may be NULL): each subband's RX
+ * output length R_tot,m L_S,m and offset in a unit's output row. */
+int fcw_cont_plan_get_info(const fcw_cont_plan* plan, fcw_cont_info* info, int64_t* rx_out_len,
+                           int64_t* rx_out_off);
+/* streams: device complex64 [S][stream_total] (subband streams concatenated
+ * in order); wave: device complex64 [S][tx_stride].  Stream-ordered. */
+int fcw_tx_continuous(const fcw_cont_plan* plan, const void* streams, void* wave, int S, void* stream);
+/* wave: device complex64 [S][rx_wave_len]; out: device complex64
+ * [S][rx_out_total], subband m at rx_out_off[m] (rx_continuous per subband). */
+int fcw_rx_continuous(const fcw_cont_plan* plan, const void* wave, void* out, int S, void* stream);
+
 /* -------------------------------------------------- host-buffer entry points */
 
 /* Same as fcw_tx / fcw_rx with HOST buffers (pinned via fcw_host_alloc for

@@ -112,6 +112,10 @@ def lib():
         L.fco_awgn.restype = None
         L.fco_measure_power.argtypes = [_f64p, C.c_int64, C.c_int64, C.c_int64]
         L.fco_measure_power.restype = C.c_double
+        L.fco_tx_continuous.argtypes = [C.c_int, C.c_double, C.c_int, _i32p, _i32p, _f64p, _f64p, _i64p, C.c_int,
+                                        _f64p, C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+        L.fco_rx_continuous.argtypes = [_f64p, C.c_int64, C.c_int, C.c_double, C.c_int, C.c_int, _f64p, _f64p,
+                                        C.c_int64, C.POINTER(C.c_int64)]
     return _lib
 
 
@@ -149,6 +153,12 @@ def ref():
         R.fcwref_evm_db.argtypes = [_f64p, _f64p, C.c_longlong, C.POINTER(C.c_double)]
         R.fcwref_awgn_with_variance.argtypes = [_f64p, C.c_longlong, C.c_double, C.c_ulonglong]
         R.fcwref_measure_power.argtypes = [_f64p, C.c_longlong, C.c_longlong, C.c_longlong, C.POINTER(C.c_double)]
+        _i64p = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
+        R.fcwref_tx_continuous.argtypes = [C.c_int, C.c_double, C.c_int, _i32p, _i32p, _f64p, _f64p, _i64p,
+                                           C.c_int, _f64p, C.c_longlong, C.POINTER(C.c_longlong),
+                                           C.POINTER(C.c_longlong)]
+        R.fcwref_rx_continuous.argtypes = [_f64p, C.c_longlong, C.c_int, C.c_double, C.c_int, C.c_int, _f64p,
+                                           _f64p, C.c_longlong, C.POINTER(C.c_longlong)]
         R.fcwref_awgn_noise_variance.argtypes = [_f64p, C.c_longlong, C.c_double, C.c_int, C.c_int,
                                                  C.POINTER(C.c_double)]
     return _ref
@@ -379,6 +389,36 @@ def measure_power(wave, begin: int, end: int) -> float:
     return float(lib().fco_measure_power(w.view(np.float64), len(w), begin, end))
 
 
+def _cont_cap(N, Ls, lens):
+    return int(max((ln + L) // (L // 2) + 3 for L, ln in zip(Ls, lens)) * (N // 2) + 2 * N)
+
+
+def tx_continuous(streams, Ls, cs, windows, N: int, overlap: float = 0.5, l_cp0: int = 0):
+    """fc_core.cpp:163-198.  streams: one complex array per subband."""
+    lens = np.array([len(x) for x in streams], np.int64)
+    flat = np.concatenate([_c128(x) for x in streams]) if len(streams) else np.zeros(0, np.complex128)
+    cap = _cont_cap(N, Ls, lens)
+    out = np.zeros(2 * cap, np.float64)
+    ol, u0 = C.c_int64(), C.c_int64()
+    _check(lib().fco_tx_continuous(N, overlap, len(Ls), _i32(Ls), _i32(cs),
+                                   np.concatenate([np.asarray(w, np.float64) for w in windows]),
+                                   flat.view(np.float64), lens, l_cp0, out, cap, C.byref(ol), C.byref(u0)),
+           "tx_continuous")
+    return out.view(np.complex128)[: ol.value].copy(), u0.value
+
+
+def rx_continuous(wave, N: int, L: int, c: int, window, overlap: float = 0.5) -> np.ndarray:
+    """fc_core.cpp:200-223 for one subband."""
+    w = _as_f64(wave)
+    n = len(w) // 2
+    cap = (n // max(1, N // L) + 2 * L) * 2 + 4 * L
+    out = np.zeros(2 * cap, np.float64)
+    no = C.c_int64()
+    _check(lib().fco_rx_continuous(w, n, N, overlap, L, c, np.asarray(window, np.float64), out, cap, C.byref(no)),
+           "rx_continuous")
+    return out.view(np.complex128)[: no.value].copy()
+
+
 def evm_db(num: float, den: float) -> float:
     """metrics.cpp:115-127 from the accumulated sums."""
     if den <= 0.0:
@@ -498,3 +538,27 @@ class Ref:
         _check(ref().fcwref_awgn_noise_variance(w.view(np.float64), len(w), snr_db, n_fft, n_active, C.byref(v)),
                "ref noise variance", ref())
         return v.value
+
+    @staticmethod
+    def tx_continuous(streams, Ls, cs, windows, N: int, overlap: float = 0.5, l_cp0: int = 0):
+        lens = np.array([len(x) for x in streams], np.int64)
+        flat = np.concatenate([_c128(x) for x in streams])
+        cap = _cont_cap(N, Ls, lens)
+        out = np.zeros(2 * cap, np.float64)
+        ol, u0 = C.c_longlong(), C.c_longlong()
+        _check(ref().fcwref_tx_continuous(N, overlap, len(Ls), _i32(Ls), _i32(cs),
+                                          np.concatenate([np.asarray(w, np.float64) for w in windows]),
+                                          flat.view(np.float64), lens, l_cp0, out, cap, C.byref(ol), C.byref(u0)),
+               "ref tx_continuous", ref())
+        return out.view(np.complex128)[: ol.value].copy(), u0.value
+
+    @staticmethod
+    def rx_continuous(wave, N: int, L: int, c: int, window, overlap: float = 0.5) -> np.ndarray:
+        w = _as_f64(wave)
+        n = len(w) // 2
+        cap = (n // max(1, N // L) + 2 * L) * 2 + 4 * L
+        out = np.zeros(2 * cap, np.float64)
+        no = C.c_longlong()
+        _check(ref().fcwref_rx_continuous(w, n, N, overlap, L, c, np.asarray(window, np.float64), out, cap,
+                                          C.byref(no)), "ref rx_continuous", ref())
+        return out.view(np.complex128)[: no.value].copy()

@@ -580,3 +580,98 @@ double fco_measure_power(const double* wave, int64_t len, int64_t begin, int64_t
     for (int64_t t = begin; t < end; ++t) p += wave[2 * t] * wave[2 * t] + wave[2 * t + 1] * wave[2 * t + 1];
     return p / (double)(end - begin);
 }
+
+/* ------------------------------------------------ continuous FC (row f2) */
+
+/* fc_core.cpp:155-161 */
+int fco_continuous_block_count(int stream_len, const fco_params* p) {
+    const int need = stream_len + p->L_O - p->L_L;
+    return (need + p->L_S - 1) / p->L_S;
+}
+
+/* fc_core.cpp:163-198 tx_continuous: per subband, the stream is padded with
+ * L_O leading zeros, cut into blocks hopping L_S, each block goes through
+ * sfb_block_ola (analysis window, synth_core with block_phase(R)) and is
+ * overlap-added at R*N_S scaled by sqrt(I); subbands are summed.
+ * streams: concatenated per subband (lens[m] complex each).  Returns 1 on the
+ * reference's invalid_argument cases; *out_len, *useful0 as the reference. */
+int fco_tx_continuous(int N, double overlap, int M, const int* Ls, const int* cs, const double* windows,
+                      const double* streams, const int64_t* lens, int l_cp0, double* wave, int64_t cap,
+                      int64_t* out_len, int64_t* useful0) {
+    if (M < 1) return 1;
+    int64_t qlen = 0;
+    size_t woff = 0, soff = 0;
+    memset(wave, 0, sizeof(double) * 2 * (size_t)cap);
+    for (int m = 0; m < M; ++m) {
+        const int L = Ls[m];
+        fco_params p;
+        if (fco_derive_params(N, L, overlap, &p)) return 1;
+        const int len = (int)lens[m];
+        const int R_tot = fco_continuous_block_count(len, &p);
+        const int64_t ol = (int64_t)(R_tot - 1) * p.N_S + p.N;
+        if (ol > cap) return 2;
+        if (ol > qlen) qlen = ol;
+        const double scale = sqrt((double)p.I);
+        double* xw = zalloc((size_t)L);
+        double* blk = zalloc((size_t)N);
+        for (int R = 0; R < R_tot; ++R) {
+            /* padded[R L_S + i] = stream[R L_S + i - L_O]; a passes [L_L, L_L + L_S) */
+            for (int i = 0; i < L; ++i) {
+                const int64_t j = (int64_t)R * p.L_S + i - p.L_O;
+                const int keep = i >= p.L_L && i < p.L_L + p.L_S && j >= 0 && j < len;
+                xw[2 * i] = keep ? streams[2 * (soff + (size_t)j)] : 0.0;
+                xw[2 * i + 1] = keep ? streams[2 * (soff + (size_t)j) + 1] : 0.0;
+            }
+            double pr, pi;
+            fco_block_phase(R, cs[m], p.L_S, L, &pr, &pi);
+            synth_block(xw, L, cs[m], windows + woff, N, pr, pi, blk);
+            for (int t = 0; t < N; ++t) {
+                wave[2 * ((int64_t)R * p.N_S + t)] += scale * blk[2 * t];
+                wave[2 * ((int64_t)R * p.N_S + t) + 1] += scale * blk[2 * t + 1];
+            }
+        }
+        if (m == 0) *useful0 = (int64_t)llround(overlap * N) + (int64_t)p.I * l_cp0;
+        free(xw);
+        free(blk);
+        woff += (size_t)L;
+        soff += (size_t)len;
+    }
+    *out_len = qlen;
+    return 0;
+}
+
+/* fc_core.cpp:200-223 rx_continuous for one subband: the waveform is
+ * prefixed with N_L zeros, blocks hop N_S, each goes through afb_block_ols
+ * with block_phase(R) and the central L_S samples (x sqrt(I)) are kept.
+ * out: R_tot * L_S complex (*n_out = that count). */
+int fco_rx_continuous(const double* wave, int64_t len, int N, double overlap, int L, int c,
+                      const double* window, double* out, int64_t cap, int64_t* n_out) {
+    fco_params p;
+    if (fco_derive_params(N, L, overlap, &p)) return 1;
+    if (len < p.N) return 1;
+    const int64_t nlow = (len + p.I - 1) / p.I + p.L;
+    const int64_t R_tot = (nlow + p.L_S - 1) / p.L_S;
+    if (R_tot * p.L_S > cap) return 2;
+    const double scale = sqrt((double)p.I);
+    double* y = zalloc((size_t)N);
+    double* z = zalloc((size_t)L);
+    for (int64_t R = 0; R < R_tot; ++R) {
+        for (int t = 0; t < N; ++t) {
+            const int64_t j = R * p.N_S + t - p.N_L;  /* x[N_L + t] = w[t] */
+            const int in = j >= 0 && j < len;
+            y[2 * t] = in ? wave[2 * j] : 0.0;
+            y[2 * t + 1] = in ? wave[2 * j + 1] : 0.0;
+        }
+        double pr, pi;
+        fco_block_phase(R, c, p.L_S, L, &pr, &pi);
+        afb_ols(y, L, c, window, &p, pr, pi, z);
+        for (int u = 0; u < p.L_S; ++u) {
+            out[2 * (R * p.L_S + u)] = scale * z[2 * (p.L_L + u)];
+            out[2 * (R * p.L_S + u) + 1] = scale * z[2 * (p.L_L + u) + 1];
+        }
+    }
+    *n_out = R_tot * p.L_S;
+    free(y);
+    free(z);
+    return 0;
+}

@@ -84,6 +84,14 @@ void fco_gauss_complex(uint64_t* state, double* re, double* im);
 void fco_awgn(double* wave, int64_t len, double sigma2, uint64_t seed);
 double fco_measure_power(const double* wave, int64_t len, int64_t begin, int64_t end);
 
+/* Continuous FC filterbank (f2): fc_core.cpp:155-223. */
+int fco_continuous_block_count(int stream_len, const fco_params* p);
+int fco_tx_continuous(int N, double overlap, int M, const int* Ls, const int* cs, const double* windows,
+                      const double* streams, const int64_t* lens, int l_cp0, double* wave, int64_t cap,
+                      int64_t* out_len, int64_t* useful0);
+int fco_rx_continuous(const double* wave, int64_t len, int N, double overlap, int L, int c,
+                      const double* window, double* out, int64_t cap, int64_t* n_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -311,4 +311,43 @@ int fcwref_awgn_noise_variance(const double* wave, long long n, double snr_db, i
     });
 }
 
+/* ---- continuous FC (f2): fc_core.hpp:64-77 ---- */
+int fcwref_tx_continuous(int N, double overlap, int M, const int* Ls, const int* cs, const double* windows,
+                         const double* streams, const long long* lens, int l_cp0, double* wave_out, long long cap,
+                         long long* out_len, long long* useful0) {
+    return guarded([&] {
+        std::vector<fcwave::CpOfdmSignal> sigs;
+        std::vector<fcwave::SubbandConfig> cfgs;
+        size_t soff = 0, woff = 0;
+        for (int m = 0; m < M; ++m) {
+            fcwave::CpOfdmSignal sg;
+            sg.samples = to_cvec(streams + 2 * soff, (std::size_t)lens[m]);
+            sg.cp_lengths = {m == 0 ? l_cp0 : 0};
+            sg.l_ofdm = Ls[m];
+            sigs.push_back(std::move(sg));
+            cfgs.push_back(cfg_of(Ls[m], cs[m], windows + woff));
+            soff += (size_t)lens[m];
+            woff += (size_t)Ls[m];
+        }
+        const fcwave::Waveform w = fcwave::tx_continuous(sigs, cfgs, N, overlap, 1.0);
+        if ((long long)w.samples.size() > cap) throw std::out_of_range("capacity");
+        from_cvec(w.samples, wave_out);
+        *out_len = (long long)w.samples.size();
+        *useful0 = (long long)w.useful0;
+    });
+}
+
+int fcwref_rx_continuous(const double* wave, long long len, int N, double overlap, int L, int c,
+                         const double* window, double* out, long long cap, long long* n_out) {
+    return guarded([&] {
+        fcwave::Waveform w;
+        w.samples = to_cvec(wave, (std::size_t)len);
+        const fcwave::FcParams p = fcwave::derive_fc_params(N, L, overlap);
+        const cvec z = fcwave::rx_continuous(w, cfg_of(L, c, window), p);
+        if ((long long)z.size() > cap) throw std::out_of_range("capacity");
+        from_cvec(z, out);
+        *n_out = (long long)z.size();
+    });
+}
+
 }  // extern "C"

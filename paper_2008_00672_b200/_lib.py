@@ -28,7 +28,15 @@ EXPORTS = [
     "fcw_nr_cp_schedule", "fcw_cp_truncate", "fcw_first_block_overlap", "fcw_design_window",
     "fcw_centered_active_map", "fcw_symbol_sigma", "fcw_combined_length", "fcw_last_error", "fcw_version",
     "fcw_link_stats", "fcw_awgn", "fcw_wave_power",
+    "fcw_cont_plan_create", "fcw_cont_plan_destroy", "fcw_cont_plan_get_info", "fcw_tx_continuous",
+    "fcw_rx_continuous",
 ]
+
+
+class ContInfoC(C.Structure):
+    _fields_ = [("N", C.c_int), ("M", C.c_int)] + [
+        (n, C.c_int64) for n in ("tx_len", "tx_stride", "useful0", "stream_total", "rx_wave_len", "rx_out_total")
+    ] + [("tx_pairs", C.c_int), ("rx_pairs", C.c_int)]
 
 
 class LinkStatC(C.Structure):
@@ -97,6 +105,13 @@ def lib() -> C.CDLL:
     L.fcw_link_stats.argtypes = [vp, vp, i64, C.c_int, C.c_uint64, i64, C.c_int, C.POINTER(LinkStatC), vp]
     L.fcw_awgn.argtypes = [vp, vp, i64, i64, C.c_int, C.c_double, C.c_uint64, i64, vp]
     L.fcw_wave_power.argtypes = [vp, vp, i64, i64, C.c_int, i64, i64, C.POINTER(C.c_double), vp]
+    L.fcw_cont_plan_create.argtypes = [C.POINTER(vp), C.c_int, C.c_double, vp, C.c_int, C.POINTER(C.c_int64), i64,
+                                       C.c_int]
+    L.fcw_cont_plan_destroy.argtypes = [vp]
+    L.fcw_cont_plan_destroy.restype = None
+    L.fcw_cont_plan_get_info.argtypes = [vp, C.POINTER(ContInfoC), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+    L.fcw_tx_continuous.argtypes = [vp, vp, vp, C.c_int, vp]
+    L.fcw_rx_continuous.argtypes = [vp, vp, vp, C.c_int, vp]
     L.fcw_tx_host.argtypes = [vp, vp, vp, C.c_int, C.c_uint]
     L.fcw_rx_host.argtypes = [vp, vp, i64, i64, vp, C.c_int, C.c_uint]
     L.fcw_host_alloc.argtypes = [C.c_size_t]

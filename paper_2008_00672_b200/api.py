@@ -446,6 +446,99 @@ def rx_discontinuous(w: Waveform, cfg: SubbandConfig, cps: CpSchedule, N: int, o
     return list(rx_discontinuous_all(w, [cfg], cps, N, overlap, simplified)[0])
 
 
+# ------------------------------------------- continuous FC filterbank (f2)
+@dataclass
+class CpOfdmSignal:  # ofdm.hpp:52-56
+    samples: np.ndarray
+    cp_lengths: list[int] = field(default_factory=list)
+    l_ofdm: int = 0
+
+
+class ContPlan:
+    """Device plan of the continuous FC filterbank (tx_continuous /
+    rx_continuous, fc_core.hpp:64-77) for fixed subbands, per-subband TX stream
+    lengths and RX waveform length; batched over S units like Plan."""
+
+    def __init__(self, N: int, subbands: Sequence[SubbandConfig], stream_len: Sequence[int], rx_wave_len: int,
+                 l_cp0: int = 0, overlap: float = 0.5):
+        self.N, self.M = N, len(subbands)
+        self.subbands = list(subbands)
+        arr = (_lib.SubbandC * max(1, self.M))()
+        for m, sb in enumerate(subbands):
+            if len(sb.window) != sb.L:
+                raise ValueError("window length must be L")
+            arr[m].L, arr[m].l_ofdm, arr[m].c = sb.L, sb.L, sb.c
+            arr[m].n_active, arr[m].n_tb = 0, sb.n_tb
+            arr[m].active_bins = None
+            arr[m].window = sb.window.ctypes.data_as(C.POINTER(C.c_double))
+        lens = (C.c_int64 * max(1, self.M))(*[int(x) for x in stream_len])
+        h = C.c_void_p()
+        check(lib().fcw_cont_plan_create(C.byref(h), N, overlap, arr, self.M, lens, int(rx_wave_len), int(l_cp0)))
+        self._h = h
+        info = _lib.ContInfoC()
+        lo = (C.c_int64 * max(1, self.M))()
+        oo = (C.c_int64 * max(1, self.M))()
+        check(lib().fcw_cont_plan_get_info(self._h, C.byref(info), lo, oo))
+        self.tx_len, self.tx_stride, self.useful0 = int(info.tx_len), int(info.tx_stride), int(info.useful0)
+        self.stream_total, self.rx_wave_len = int(info.stream_total), int(info.rx_wave_len)
+        self.rx_out_total = int(info.rx_out_total)
+        self.rx_out_len = [int(lo[m]) for m in range(self.M)]
+        self.rx_out_off = [int(oo[m]) for m in range(self.M)]
+        self.stream_len = [int(x) for x in stream_len]
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib().fcw_cont_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def tx(self, streams, wave, S: int, stream=None) -> None:
+        """streams: device complex64 [S][stream_total]; wave: [S][tx_stride]."""
+        check(lib().fcw_tx_continuous(self._h, _dev_ptr(streams), _dev_ptr(wave), S, _stream_ptr(stream)))
+
+    def rx(self, wave, out, S: int, stream=None) -> None:
+        """wave: device complex64 [S][rx_wave_len]; out: [S][rx_out_total]."""
+        check(lib().fcw_rx_continuous(self._h, _dev_ptr(wave), _dev_ptr(out), S, _stream_ptr(stream)))
+
+
+def tx_continuous(signals: Sequence[CpOfdmSignal], cfgs: Sequence[SubbandConfig], N: int, overlap: float,
+                  fs_hz: float) -> Waveform:
+    """fc_core.hpp:71-73 on the GPU (one unit, host arrays)."""
+    import torch
+
+    if len(signals) != len(cfgs) or not signals:
+        raise ValueError("one config per subband signal required")  # fc_core.cpp:166
+    lens = [len(sg.samples) for sg in signals]
+    l_cp0 = signals[0].cp_lengths[0] if signals[0].cp_lengths else 0
+    p = ContPlan(N, cfgs, lens, max(N, 1), l_cp0, overlap)
+    flat = np.concatenate([np.asarray(sg.samples, np.complex64) for sg in signals])
+    d_in = torch.from_numpy(flat).cuda()
+    d_out = torch.empty(p.tx_stride, dtype=torch.complex64, device="cuda")
+    p.tx(d_in, d_out, 1)
+    torch.cuda.synchronize()
+    return Waveform(d_out.cpu().numpy()[: p.tx_len].astype(np.complex128), fs_hz, p.useful0)
+
+
+def rx_continuous(w: Waveform, cfg: SubbandConfig, p: FcParams) -> np.ndarray:
+    """fc_core.hpp:77 on the GPU for one subband (p: derive_fc_params)."""
+    import torch
+
+    n = len(w.samples)
+    if n < p.N:
+        raise ValueError("waveform shorter than one FC block")  # fc_core.cpp:201
+    cp = ContPlan(p.N, [cfg], [0], n, 0, p.overlap)
+    d_w = torch.from_numpy(np.asarray(w.samples, np.complex64)).cuda()
+    d_o = torch.empty(cp.rx_out_total, dtype=torch.complex64, device="cuda")
+    cp.rx(d_w, d_o, 1)
+    torch.cuda.synchronize()
+    return d_o.cpu().numpy().astype(np.complex128)
+
+
 # ------------------------------------------------------------ link metrics
 @dataclass
 class LinkStats:

@@ -100,6 +100,12 @@ void pick_schedule(const fcw::Plan& p, int S, bool tx, fcw::KParams& kp) {
 
 }  // namespace
 
+namespace fcw {
+// shared with the other C-ABI translation units (fcw_cont.cu)
+int set_error(int code, const std::string& msg) { return fail(code, msg); }
+int set_cuda_error(cudaError_t e, const char* where) { return cuda_fail(e, where); }
+}  // namespace fcw
+
 struct fcw_plan : fcw::Plan {};
 
 extern "C" {

@@ -130,6 +130,22 @@ struct Plan {
     size_t stage_bytes[2][2] = {{0, 0}, {0, 0}};
 };
 
+// Continuous-FC column descriptor (fcw_cont.cu): one per subband.
+struct fc_col {
+    long long in_off;   // TX: offset of this subband's stream in a unit's concatenated streams
+    long long len;      // TX: stream length (low-rate samples)
+    long long out_off;  // RX: offset of this subband's output stream in a unit's output
+    long long len_out;  // RX: R_tot * L_S output samples
+    int lt;             // L_T: the block-pair window starts L_T samples before 2 n L_S
+    int row;            // full grid row length (sum L_m)
+    int full_off;       // this subband's first bin in a full grid row
+    int pad_;
+};
+
+int set_error(int code, const std::string& msg);
+struct fc_col;
+int set_cuda_error(cudaError_t e, const char* where);
+
 // fcw_launch.cu
 cudaError_t launch_tx(const Plan& plan, KParams& kp, int S, cudaStream_t st);
 cudaError_t launch_rx(const Plan& plan, KParams& kp, int S, cudaStream_t st);
