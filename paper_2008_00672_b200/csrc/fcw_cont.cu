@@ -356,7 +356,7 @@ int fcw_tx_continuous(const fcw_cont_plan* p, const void* streams, void* wave, i
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const long long grid_stride = (long long)p->B_tx * p->row_full;
     float2* grid = nullptr;
-    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&grid), sizeof(float2) * grid_stride * S, st);
+    cudaError_t e = fcw::scratch_alloc(&grid, sizeof(float2) * grid_stride * S, st);
     if (e != cudaSuccess) return fcw::set_cuda_error(e, "continuous TX scratch");
     int rc = FCW_OK;
     for (int u0 = 0; u0 < S && rc == FCW_OK; u0 += 65535) {
@@ -383,8 +383,8 @@ int fcw_rx_continuous(const fcw_cont_plan* p, const void* wave, void* out, int S
     const long long grid_stride = (long long)p->B_rx * p->row_full;
     const long long pad = p->rx_pad_len;
     float2 *wp = nullptr, *grid = nullptr;
-    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&wp), sizeof(float2) * pad * S, st);
-    if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&grid), sizeof(float2) * grid_stride * S, st);
+    cudaError_t e = fcw::scratch_alloc(&wp, sizeof(float2) * pad * S, st);
+    if (e == cudaSuccess) e = fcw::scratch_alloc(&grid, sizeof(float2) * grid_stride * S, st);
     if (e == cudaSuccess) e = cudaMemsetAsync(wp, 0, sizeof(float2) * pad * S, st);
     // x = [0_{N_L}, w, 0 ...] (fc_core.cpp:207-208)
     if (e == cudaSuccess)

@@ -147,6 +147,18 @@ struct fc_col;
 int set_cuda_error(cudaError_t e, const char* where);
 
 // fcw_launch.cu
+// per-device stream-ordered scratch pool that keeps its memory (no OS
+// re-allocation after every synchronisation)
+cudaError_t scratch_pool(int dev, cudaMemPool_t* out);
+template <class T>
+cudaError_t scratch_alloc(T** p, size_t bytes, cudaStream_t st) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (e == cudaSuccess) e = scratch_pool(dev, &pool);
+    if (e == cudaSuccess) e = cudaMallocFromPoolAsync(reinterpret_cast<void**>(p), bytes, pool, st);
+    return e;
+}
 cudaError_t launch_tx(const Plan& plan, KParams& kp, int S, cudaStream_t st);
 cudaError_t launch_rx(const Plan& plan, KParams& kp, int S, cudaStream_t st);
 cudaError_t launch_gen_qam(const Plan& plan, uint64_t seed, long long unit0, int S, int bits,

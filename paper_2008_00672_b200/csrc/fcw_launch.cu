@@ -126,33 +126,6 @@ size_t smem_bytes(const Plan& p, bool tx, bool rx_direct) {
 // Persistent launch: as many CTAs as can be resident; each team owns a static
 // balanced range of the S*B symbols.  The TX carry buffers are per-launch
 // stream-ordered scratch, so concurrent launches never share them.
-// Per-device stream-ordered pool that keeps freed memory (release threshold
-// = max): the per-launch scratch is then a sub-microsecond pool hit instead of
-// an OS allocation after every synchronisation.
-cudaError_t scratch_pool(int dev, cudaMemPool_t* out) {
-    static std::mutex mu;
-    static std::map<int, cudaMemPool_t> pools;
-    std::lock_guard<std::mutex> lk(mu);
-    auto it = pools.find(dev);
-    if (it != pools.end()) {
-        *out = it->second;
-        return cudaSuccess;
-    }
-    cudaMemPoolProps props{};
-    props.allocType = cudaMemAllocationTypePinned;
-    props.location.type = cudaMemLocationTypeDevice;
-    props.location.id = dev;
-    cudaMemPool_t pool;
-    cudaError_t e = cudaMemPoolCreate(&pool, &props);
-    if (e != cudaSuccess) return e;
-    uint64_t keep = UINT64_MAX;
-    e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-    if (e != cudaSuccess) return e;
-    pools[dev] = pool;
-    *out = pool;
-    return cudaSuccess;
-}
-
 // Resident CTAs per SM for (kernel, smem, device); sets the dynamic-SMEM
 // attribute once.  Cached: the queries cost host time on every launch.
 cudaError_t resident_per_sm(KernelFn k, size_t smem, int dev, int* per_sm) {
@@ -206,6 +179,33 @@ cudaError_t launch_one(KernelFn k, size_t smem, KParams& kp, bool tx, int N, int
 }
 
 }  // namespace
+
+// Per-device stream-ordered pool that keeps freed memory (release threshold
+// = max): the per-launch scratch is then a sub-microsecond pool hit instead of
+// an OS allocation after every synchronisation.
+cudaError_t scratch_pool(int dev, cudaMemPool_t* out) {
+    static std::mutex mu;
+    static std::map<int, cudaMemPool_t> pools;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = pools.find(dev);
+    if (it != pools.end()) {
+        *out = it->second;
+        return cudaSuccess;
+    }
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t pool;
+    cudaError_t e = cudaMemPoolCreate(&pool, &props);
+    if (e != cudaSuccess) return e;
+    uint64_t keep = UINT64_MAX;
+    e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    if (e != cudaSuccess) return e;
+    pools[dev] = pool;
+    *out = pool;
+    return cudaSuccess;
+}
 
 void fill_common(const Plan& p, KParams& kp) {
     kp.N = p.N;

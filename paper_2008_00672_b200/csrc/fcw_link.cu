@@ -22,7 +22,7 @@ namespace fcw {
 namespace {
 
 constexpr int kLinkThreads = 256;
-constexpr int kLinkPerThread = 8;
+constexpr int kLinkPerThread = 32;
 constexpr long long kLinkChunk = (long long)kLinkThreads * kLinkPerThread;
 constexpr uint64_t kGamma = 0x9e3779b97f4a7c15ULL;
 
@@ -171,7 +171,7 @@ template <class Launch>
 cudaError_t reduce_to_host(int S, int chunks, cudaStream_t st, Launch&& launch, Acc* host) {
     Acc* d = nullptr;
     const size_t nparts = (size_t)S * chunks;
-    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&d), (nparts + S) * sizeof(Acc), st);
+    cudaError_t e = scratch_alloc(&d, (nparts + S) * sizeof(Acc), st);
     if (e != cudaSuccess) return e;
     launch(d);
     reduce_parts_kernel<<<(S + 127) / 128, 128, 0, st>>>(d, chunks, S, d + nparts);
