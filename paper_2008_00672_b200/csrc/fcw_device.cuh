@@ -491,11 +491,154 @@ FCW_DI void tx_short_one(const KParams& P, const Team& tm, const SymDev& sy, con
     }
 }
 
+// Sub-teams per CTA: the long transform of one block needs N/16 threads, so a
+// 256-thread CTA runs 4096/N independent teams for 512 <= N <= 4096 (each with
+// its own spectra, work items and named barrier); smaller N use one team.
+template <int N>
+constexpr int teams_per_cta() {
+    return (N >= 512 && N <= 4096) ? 4096 / N : 1;
+}
+
+// ----------------------------------------------- team-wide short transforms
+// For few large subbands (M <= warps/2, L >= 512: config 3's single L = 1024 /
+// L = 512 banks) one warp per subband would leave the team's other warps
+// idle; here the whole team transforms each subband, PPT = L / TT points per
+// thread in the cyclic distribution v[k] = x[t + TT k], through the team's
+// warp scratch (two buffers) with the team's barrier.
+// Uniform L >= 512 kernels transform on the whole team when that leaves at
+// least 4 points per thread (a warp per subband would need 16-32 points per
+// lane and spill); N = 4096 with L = 512 keeps the warp path.
+template <int N, int LU>
+constexpr bool use_team_short() {
+    return LU >= 512 && LU <= N && LU / (teams_per_cta<N>() == 1 ? kThreads : N / kPPT) >= 4;
+}
+
+template <int G>
+FCW_DI int team_bar_id(const Team& tm) {
+    return G == 1 ? 0 : 1 + (int)(threadIdx.x / tm.nthr);
+}
+
+template <int N, int L, int G>
+FCW_DI void tx_short_team(const KParams& P, const Team& tm, const SymDev& sy, const float2* __restrict__ row,
+                          float2* spec0, float2* spec1, float2* scr) {
+    constexpr int TT = G == 1 ? kThreads : N / kPPT;  // threads per team
+    constexpr int PPT = L / TT;
+    static_assert(PPT >= 4 && PPT % 4 == 0 && PPT <= 16, "team short path: L / team size");
+    const int t = tm.tid, bid = team_bar_id<G>(tm);
+    float2* sbuf = scr - tm.warp * P.scratch_stride;  // the team's warp scratch, contiguous
+    float2* const b1[1] = {sbuf};
+    float2* const b2[2] = {sbuf, sbuf + (L + L / 16 + 2)};
+    for (int m = 0; m < P.M; ++m) {
+        const SubDev sd = P.sub[m];
+        const float2 ph = cscale(tw_conj(P.tw, theta_exp<N>(sd.cmodN, sy.smodN)), sd.tx_scale);
+        float2 v[1][PPT];
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) {
+            const int b = t + TT * k;
+            v[0][k] = cmul(grid_val(P, sd, row, b, bin_entry<N, L>(P, sd, b).inv), ph);
+        }
+        team_fft<L, TT, PPT, +1, 1, true>(v, b1, P.tw, N / L, t, true, bid, TT);  // ofdm_modulate
+        const int lcp = sy.cp >> sd.logI;
+        float2 uu[2][PPT];
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) {
+            // block windows of tx_symbol (fc_sync.cpp:34-84): L/4 = (PPT/4) TT, a register rename
+            const int e = t + TT * k;
+            const bool in0 = (e >= L / 4 - lcp) && (e < 3 * L / 4);
+            const bool in1 = (e >= L / 4) && (e < 3 * L / 4);
+            uu[0][k] = in0 ? v[0][(k - PPT / 4 + PPT) % PPT] : zero2();
+            uu[1][k] = in1 ? v[0][(k + PPT / 4) % PPT] : zero2();
+        }
+        team_bar<true>(bid, TT);  // the IDFT's last exchange has been read before the DFTs reuse the buffers
+        team_fft<L, TT, PPT, -1, 2, true>(uu, b2, P.tw, N / L, t, true, bid, TT);
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) {
+            const Bin e = bin_entry<N, L>(P, sd, t + TT * k);
+            if (e.dest >= 0) {
+                spec0[e.dest] = cscale(uu[0][k], e.w);
+                spec1[e.dest] = cscale(uu[1][k], e.w * sd.bp1);
+            }
+        }
+        team_bar<true>(bid, TT);  // next subband reuses the buffers
+    }
+}
+
+// RX of one subband by the whole team, as tx_short_team: fused Eq. (30)
+// (fc_sync.cpp:195-243) or the direct path.
+template <int N, int L, int G, bool FUSED>
+FCW_DI void rx_short_team(const KParams& P, const Team& tm, const SymDev& sy, const float2* spec0,
+                          const float2* spec1, float2* __restrict__ orow, float2* scr) {
+    constexpr int TT = G == 1 ? kThreads : N / kPPT;
+    constexpr int PPT = L / TT;
+    static_assert(PPT >= 4 && PPT % 4 == 0 && PPT <= 16, "team short path: L / team size");
+    const int t = tm.tid, bid = team_bar_id<G>(tm);
+    float2* sbuf = scr - tm.warp * P.scratch_stride;
+    float2* const b1[1] = {sbuf};
+    float2* const b2[2] = {sbuf, sbuf + (L + L / 16 + 2)};
+    for (int m = 0; m < P.M; ++m) {
+        const SubDev sd = P.sub[m];
+        float2 g0[1][PPT], g1[PPT];
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) {
+            // rx_block_freq (fc_sync.cpp:178-193); b = t (mod 4) since TT is a multiple of 4
+            const int b = t + TT * k;
+            const float w = bin_entry<N, L>(P, sd, b).w;
+            const int q = (sd.c - L / 2 + (b ^ (L / 2))) & (N - 1);
+            const float2 a = cscale(spec0[q], w);
+            float2 c1 = cscale(spec1[q], w * sd.bp1);
+            if (t & 1) c1 = make_float2(-c1.x, -c1.y);  // t = Omega_{L/2} g1
+            g1[k] = c1;
+            g0[0][k] = mul_jpow_rt(csub(a, c1), t & 3);  // f = Omega_{-L/4}(g0 - t)
+        }
+        const float2 ph = __ldg(&P.tw[theta_exp<N>(sd.cmodN, sy.smodN)]);  // conj(theta_n)
+        const float a = sd.rx_s0 / (float)L, s = sd.rx_s0;
+        if (!FUSED) {
+            // direct path (rx_symbol_direct fc_sync.cpp:158-176): both analysis
+            // blocks, central halves (L/4 = (PPT/4) TT: register renames), OFDM DFT
+            float2 gg[2][PPT];
+#pragma unroll
+            for (int k = 0; k < PPT; ++k) {
+                const float2 c1 = (t & 1) ? make_float2(-g1[k].x, -g1[k].y) : g1[k];  // undo Omega_{L/2}
+                gg[1][k] = c1;
+                // g0 = f-rotation undone: a = j^{-t} f + t  ->  recover a from f and c1
+                gg[0][k] = cadd(mul_jpow_rt(g0[0][k], (4 - (t & 3)) & 3), g1[k]);
+            }
+            team_fft<L, TT, PPT, +1, 2, true>(gg, b2, P.tw, N / L, t, true, bid, TT);
+#pragma unroll
+            for (int k = 0; k < PPT; ++k)
+                g0[0][k] = k < PPT / 2 ? gg[0][k + PPT / 4] : gg[1][k - PPT / 4];
+            team_bar<true>(bid, TT);
+            team_fft<L, TT, PPT, -1, 1, true>(g0, b1, P.tw, N / L, t, true, bid, TT);
+        } else {
+            team_fft<L, TT, PPT, +1, 1, true>(g0, b1, P.tw, N / L, t, true, bid, TT);
+#pragma unroll
+            for (int k = PPT / 2; k < PPT; ++k) g0[0][k] = zero2();  // S-hat: e >= L/2
+            team_bar<true>(bid, TT);
+            team_fft<L, TT, PPT, -1, 1, true>(g0, b1, P.tw, N / L, t, true, bid, TT);
+        }
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) {
+            const int b = t + TT * k;
+            const float2 tj = FUSED ? mul_jpow_rt(g1[k], t & 3) : zero2();
+            const float2 o = cmul(make_float2(fmaf(g0[0][k].x, a, tj.x * s), fmaf(g0[0][k].y, a, tj.y * s)), ph);
+            if (P.grid_full) {
+                orow[sd.full_off + b] = o;
+            } else {
+                const int inv = bin_entry<N, L>(P, sd, b).inv;
+                if (inv >= 0) orow[sd.act_off + inv] = o;
+            }
+        }
+        team_bar<true>(bid, TT);
+    }
+}
+
 template <int N, int LU>
 FCW_DI void tx_short_all(const KParams& P, const Team& tm, const SymDev& sy, const float2* __restrict__ row,
                          const float2* __restrict__ row_next, bool staged, float2* spec0, float2* spec1,
                          float2* scr, const float2* stw) {
-    if constexpr (LU > 0) {
+    if constexpr (use_team_short<N, LU>()) {
+        tx_short_team<N, LU, teams_per_cta<N>()>(P, tm, sy, row, spec0, spec1, scr);
+    } else if constexpr (LU > 0) {
         // uniform L: the next symbol's first subband is staged across calls
         tx_short_one<N, LU>(P, tm, sy, row, row_next, staged, spec0, spec1, scr, stw, 0, P.M);
     } else {
@@ -772,7 +915,12 @@ FCW_DI void rx_short_one(const KParams& P, const Team& tm, const SymDev& sy, con
 template <int N, int LU>
 FCW_DI void rx_short_all(const KParams& P, const Team& tm, const SymDev& sy, const float2* spec0,
                          const float2* spec1, float2* orow, float2* scr, const float2* stw) {
-    if constexpr (LU > 0) {
+    if constexpr (use_team_short<N, LU>()) {
+        if (P.fused)
+            rx_short_team<N, LU, teams_per_cta<N>(), true>(P, tm, sy, spec0, spec1, orow, scr);
+        else
+            rx_short_team<N, LU, teams_per_cta<N>(), false>(P, tm, sy, spec0, spec1, orow, scr);
+    } else if constexpr (LU > 0) {
         rx_short_one<N, LU, LU == 256>(P, tm, sy, spec0, spec1, orow, scr, stw, 0, P.M);
     } else {
         for (int g = 0; g < P.n_groups; ++g) {
@@ -800,13 +948,6 @@ constexpr int min_blocks() {
     return (LU >= 64 || (LU > 0 && LU <= 16)) ? 2 : 1;
 }
 
-// Sub-teams per CTA: the long transform of one block needs N/16 threads, so a
-// 256-thread CTA runs 4096/N independent teams for 512 <= N <= 4096 (each with
-// its own spectra, work items and named barrier); smaller N use one team.
-template <int N>
-constexpr int teams_per_cta() {
-    return (N >= 512 && N <= 4096) ? 4096 / N : 1;
-}
 
 // Team-scope barrier: the CTA barrier for a single team, else named barrier
 // 1 + g over the team's threads (bar.sync counts must be warp multiples).
