@@ -505,9 +505,9 @@ constexpr int teams_per_cta() {
 // idle; here the whole team transforms each subband, PPT = L / TT points per
 // thread in the cyclic distribution v[k] = x[t + TT k], through the team's
 // warp scratch (two buffers) with the team's barrier.
-// Uniform L >= 512 kernels transform on the whole team when that leaves at
-// least 4 points per thread (a warp per subband would need 16-32 points per
-// lane and spill); N = 4096 with L = 512 keeps the warp path.
+// Uniform L >= 512 kernels may transform on the whole team (when that leaves
+// at least 4 points per thread); they do so when the plan has at most one
+// subband per two warps of a team (config 3), else one warp per subband.
 template <int N, int LU>
 constexpr bool use_team_short() {
     return LU >= 512 && LU <= N && LU / (teams_per_cta<N>() == 1 ? kThreads : N / kPPT) >= 4;
@@ -637,7 +637,11 @@ FCW_DI void tx_short_all(const KParams& P, const Team& tm, const SymDev& sy, con
                          const float2* __restrict__ row_next, bool staged, float2* spec0, float2* spec1,
                          float2* scr, const float2* stw) {
     if constexpr (use_team_short<N, LU>()) {
-        tx_short_team<N, LU, teams_per_cta<N>()>(P, tm, sy, row, spec0, spec1, scr);
+        // few subbands: the whole team per subband; else one warp per subband
+        if (2 * P.M <= tm.nwarp)
+            tx_short_team<N, LU, teams_per_cta<N>()>(P, tm, sy, row, spec0, spec1, scr);
+        else
+            tx_short_one<N, LU>(P, tm, sy, row, row_next, staged, spec0, spec1, scr, stw, 0, P.M);
     } else if constexpr (LU > 0) {
         // uniform L: the next symbol's first subband is staged across calls
         tx_short_one<N, LU>(P, tm, sy, row, row_next, staged, spec0, spec1, scr, stw, 0, P.M);
@@ -916,7 +920,9 @@ template <int N, int LU>
 FCW_DI void rx_short_all(const KParams& P, const Team& tm, const SymDev& sy, const float2* spec0,
                          const float2* spec1, float2* orow, float2* scr, const float2* stw) {
     if constexpr (use_team_short<N, LU>()) {
-        if (P.fused)
+        if (2 * P.M > tm.nwarp)
+            rx_short_one<N, LU>(P, tm, sy, spec0, spec1, orow, scr, stw, 0, P.M);
+        else if (P.fused)
             rx_short_team<N, LU, teams_per_cta<N>(), true>(P, tm, sy, spec0, spec1, orow, scr);
         else
             rx_short_team<N, LU, teams_per_cta<N>(), false>(P, tm, sy, spec0, spec1, orow, scr);
