@@ -91,9 +91,11 @@ void pick_schedule(const fcw::Plan& p, int S, bool tx, fcw::KParams& kp) {
     const int G = (p.N >= 512 && p.N <= 4096) ? 4096 / p.N : 1;
     const long long teams = 2LL * 148 * G;
     const long long per_team = (long long)p.B * std::max(S, 1) / teams;
-    if (!kp.dynamic && per_team >= 200) {
+    const char* sched = std::getenv("FCW_SCHED");  // dev A/B knob: "static" keeps balanced static ranges
+    const bool force_static = sched && std::strcmp(sched, "static") == 0;
+    if (!kp.dynamic && per_team >= 200 && !force_static) {
         kp.dynamic = 1;
-        kp.chunk = std::min(p.B, tx ? 28 : 16);
+        kp.chunk = std::min(p.B, tx ? 140 : 16);  // measured (tools/tools_sched.sh): TX 28 -> 140 is -1%
     }
     kp.nchunks = (p.B + kp.chunk - 1) / kp.chunk;
 }

@@ -104,17 +104,11 @@ FCW_DI float2 zero2() { return make_float2(0.f, 0.f); }
 
 constexpr int kLtwLen = 64 + 4096 / 64;  // two-level long-transform twiddles (SMEM)
 constexpr int kTw16Len = 512;            // fft256_half per-lane twiddles (uniform L = 256 kernels)
-#ifndef FCW_TX_HALF
-#define FCW_TX_HALF 1  // TX L = 256 on half-warps (tail on whole warps) vs whole-warp lockstep
-#endif
 #ifndef FCW_RX_HYBRID
 #define FCW_RX_HYBRID 0  // fused RX L = 256: whole-warp tail round
 #endif
-#ifndef FCW_TX_DST1
-#define FCW_TX_DST1 0  // TX half-warp scatter: decode bin destinations once for both blocks
-#endif
-#ifndef FCW_TX_LS
-#define FCW_TX_LS 0  // TX half-warp: both block DFTs in lockstep
+#ifndef FCW_TX_TAIL2
+#define FCW_TX_TAIL2 1  // TX half-warp tail round: one subband per warp, one block per half
 #endif
 #ifndef FCW_TW16
 #define FCW_TW16 1
@@ -362,14 +356,18 @@ FCW_DI void tx_short_half(const KParams& P, const Team& tm, const SymDev& sy, co
     static_assert(L == 256, "half-warp path is built for L = 256");
     const int lane = threadIdx.x & 31, t = lane & (TW - 1), h = lane >> 4;
     float2* buf = scr + h * (P.scratch_stride / 2);
-    // Rounds of 2 subbands per warp while more than one per warp remain; the
-    // tail (at most one per warp) runs on whole warps, which finish a subband
-    // in fewer dependent steps (balance: 23 subbands = 16 + 7, not 16 + 16).
+    // Pair rounds while more than one subband per warp remains: one subband
+    // per half-warp, both blocks.  Tail round (at most one subband per warp):
+    // both halves transform the same subband (redundant IDFT) and each half
+    // one block, so the tail's dependent chain is two transforms, not three
+    // (balance: 23 subbands = 16 + 7).
     int done = 0;
-    while (gcount - done > tm.nwarp) {
-        const int i = done + 2 * tm.warp + h;
-        done += 2 * tm.nwarp;
+    while (done < gcount) {
+        const bool pair = gcount - done > (FCW_TX_TAIL2 ? tm.nwarp : 0);
+        const int i = pair ? done + 2 * tm.warp + h : done + tm.warp;
+        done += pair ? 2 * tm.nwarp : tm.nwarp;
         const bool act = i < gcount;
+        if (!pair && !act) break;  // warp-uniform in the tail
         const int m = act ? (P.grp_sub ? __ldg(&P.grp_sub[gstart + i]) : gstart + i) : gstart;
         const SubDev sd = P.sub[m];
         const int2* ce = P.cls + sd.cls_off + t;
@@ -396,25 +394,24 @@ FCW_DI void tx_short_half(const KParams& P, const Team& tm, const SymDev& sy, co
         fft256_half<+1>(v, buf, stw, t, 0, tw16_of(P, stw));  // x[t + 16 m] (scales folded into ph)
         const int lcp = sy.cp >> sd.logI;
         const int qbase = sd.c - L / 2 + t, ext0 = N + sd.ext_base;
-#if FCW_TX_DST1
-        // destination slot and weight of each bin, decoded once for both blocks
-        int dst[PPT];
-        float wgt[PPT];
-        static_for<PPT>([&](auto kc) {
-            constexpr int K = decltype(kc)::value;
-            constexpr int KP = K ^ (PPT / 2);  // (t + 16K) ^ (L/2) == t + 16*KP
-            const int2 e = __ldg(&ce[TW * K]);
-            const int sec = e.x >> 16;
-            dst[K] = !act ? -1 : sec >= 0 ? ext0 + sec : (sec == -1 ? ((qbase + TW * KP) & (N - 1)) : -1);
-            wgt[K] = __int_as_float(e.y);
-        });
-        auto scatter = [&](float2 (&u)[PPT], float2* spec, float sgn) {
+        const int r0 = pair ? 0 : h, r1 = pair ? 2 : h + 1;
+#pragma unroll 1
+        for (int r = r0; r < r1; ++r) {
+            // block 0: e = t + 16 m in [L/4 - lcp, 3L/4) holds x[(e - L/4) mod L] = v[(m - 4) mod 16];
+            // block 1: e in [L/4, 3L/4) holds x[e + L/4] = v[m + 4]  (register renames, L/4 = 4 * 16)
+            float2 u[PPT];
 #pragma unroll
-            for (int K = 0; K < PPT; ++K)
-                if (dst[K] >= 0) spec[dst[K]] = cscale(u[K], wgt[K] * sgn);
-        };
-#else
-        auto scatter = [&](float2 (&u)[PPT], float2* spec, float sgn) {
+            for (int k = 0; k < PPT; ++k) {
+                if (k >= 4 && k < 12)
+                    u[k] = r ? v[k + 4] : v[k - 4];
+                else if (k < 4)
+                    u[k] = (r == 0 && t + TW * k >= L / 4 - lcp) ? v[k + 12] : zero2();
+                else
+                    u[k] = zero2();  // k >= 12: known zero (not read)
+            }
+            fft256_half<-1, 0xF000ull>(u, buf, stw, t, 0, tw16_of(P, stw));
+            float2* spec = r ? spec1 : spec0;
+            const float sgn = r ? sd.bp1 : 1.f;
             static_for<PPT>([&](auto kc) {
                 constexpr int K = decltype(kc)::value;
                 constexpr int KP = K ^ (PPT / 2);  // (t + 16K) ^ (L/2) == t + 16*KP
@@ -423,66 +420,20 @@ FCW_DI void tx_short_half(const KParams& P, const Team& tm, const SymDev& sy, co
                 const int dest = sec >= 0 ? ext0 + sec : (sec == -1 ? ((qbase + TW * KP) & (N - 1)) : -1);
                 if (act && dest >= 0) spec[dest] = cscale(u[K], __int_as_float(e.y) * sgn);
             });
-        };
-#endif
-#if FCW_TX_LS
-        {
-            // block 0: e = t + 16 m in [L/4 - lcp, 3L/4) holds x[(e - L/4) mod L] = v[(m - 4) mod 16];
-            // block 1: e in [L/4, 3L/4) holds x[e + L/4] = v[m + 4]; both DFTs in lockstep
-            float2 u0[PPT], u1[PPT];
-#pragma unroll
-            for (int k = 0; k < PPT; ++k) {
-                if (k >= 4 && k < 12)
-                    u0[k] = v[k - 4];
-                else if (k < 4)
-                    u0[k] = (t + TW * k >= L / 4 - lcp) ? v[k + 12] : zero2();
-                else
-                    u0[k] = zero2();  // k >= 12: known zero (not read)
-                u1[k] = (k >= 4 && k < 12) ? v[k + 4] : zero2();
-            }
-            fft256_half2<-1, 0xF000ull, 0xF00Full>(u0, u1, buf, t, tw16_of(P, stw));
-            scatter(u0, spec0, 1.f);
-            scatter(u1, spec1, sd.bp1);
         }
     }
-#else
-        {
-            // block 0: e = t + 16 m in [L/4 - lcp, 3L/4) holds x[(e - L/4) mod L] = v[(m - 4) mod 16]
-            float2 u[PPT];
-#pragma unroll
-            for (int k = 0; k < PPT; ++k) {
-                if (k >= 4 && k < 12)
-                    u[k] = v[k - 4];
-                else if (k < 4)
-                    u[k] = (t + TW * k >= L / 4 - lcp) ? v[k + 12] : zero2();
-                else
-                    u[k] = zero2();  // k >= 12: known zero (not read)
-            }
-            fft256_half<-1, 0xF000ull>(u, buf, stw, t, 0, tw16_of(P, stw));
-            scatter(u, spec0, 1.f);
-        }
-        {
-            // block 1: e in [L/4, 3L/4) holds x[e + L/4] = v[m + 4]
-            float2 u[PPT];
-#pragma unroll
-            for (int k = 0; k < PPT; ++k) u[k] = (k >= 4 && k < 12) ? v[k + 4] : zero2();
-            fft256_half<-1, 0xF00Full>(u, buf, stw, t, 0, tw16_of(P, stw));
-            scatter(u, spec1, sd.bp1);
-        }
-    }
-#endif
-    if (done < gcount)
-        tx_short_warp_lockstep<N, L>(P, tm, sy, row, spec0, spec1, scr, stw, gstart + done, gcount - done);
 }
 
-template <int N, int L>
+// HALF: the kernel carries the half-warp twiddle table (the uniform L = 256
+// specialisation); generic kernels use the whole-warp lockstep path.
+template <int N, int L, bool HALF = false>
 FCW_DI void tx_short_one(const KParams& P, const Team& tm, const SymDev& sy, const float2* __restrict__ row,
                          const float2* __restrict__ row_next, bool staged, float2* spec0, float2* spec1,
                          float2* scr, const float2* stw, int gs, int gc) {
     if constexpr (L <= N) {
         if constexpr (L <= 32)
             tx_short_thread<N, L>(P, tm, sy, row, spec0, spec1, gs, gc);
-        else if constexpr (L == 256 && FCW_TX_HALF)
+        else if constexpr (L == 256 && HALF)
             tx_short_half<N, L>(P, tm, sy, row, spec0, spec1, scr, stw, gs, gc);
         else if constexpr (L <= 256)
             tx_short_warp_lockstep<N, L>(P, tm, sy, row, spec0, spec1, scr, stw, gs, gc);
@@ -644,7 +595,7 @@ FCW_DI void tx_short_all(const KParams& P, const Team& tm, const SymDev& sy, con
             tx_short_one<N, LU>(P, tm, sy, row, row_next, staged, spec0, spec1, scr, stw, 0, P.M);
     } else if constexpr (LU > 0) {
         // uniform L: the next symbol's first subband is staged across calls
-        tx_short_one<N, LU>(P, tm, sy, row, row_next, staged, spec0, spec1, scr, stw, 0, P.M);
+        tx_short_one<N, LU, LU == 256>(P, tm, sy, row, row_next, staged, spec0, spec1, scr, stw, 0, P.M);
     } else {
         for (int g = 0; g < P.n_groups; ++g) {
             const int gs = P.grp_start[g], gc = P.grp_count[g];

@@ -398,36 +398,4 @@ FCW_DI void fft256_half(float2 (&v)[16], float2* buf, const float2* stw, int t, 
     fft_reg<16, SIGN>(v);
 }
 
-// Two half-warp FFT_256s in lockstep (independent chains for ILP, shared
-// twiddle loads); the exchanges go through the one buffer in turn.
-template <int SIGN, unsigned long long Z0, unsigned long long Z1>
-FCW_DI void fft256_half2(float2 (&a)[16], float2 (&b)[16], float2* buf, int t, const float2* tw16) {
-    fft_reg<16, SIGN, Z0>(a);
-    fft_reg<16, SIGN, Z1>(b);
-    float2* wp = buf + 17 * t;
-    const float2* rp = buf + t;
-    __syncwarp();
-#pragma unroll
-    for (int k = 0; k < 16; ++k) wp[k] = a[k];
-    __syncwarp();
-#pragma unroll
-    for (int m = 0; m < 16; ++m) a[m] = rp[17 * m];
-    __syncwarp();
-#pragma unroll
-    for (int k = 0; k < 16; ++k) wp[k] = b[k];
-    __syncwarp();
-#pragma unroll
-    for (int m = 0; m < 16; ++m) b[m] = rp[17 * m];
-    const float2* tp = tw16 + t;
-#pragma unroll
-    for (int m = 1; m < 16; ++m) {
-        float2 w = tp[16 * m];
-        if constexpr (SIGN > 0) w.y = -w.y;
-        a[m] = cmul(a[m], w);
-        b[m] = cmul(b[m], w);
-    }
-    fft_reg<16, SIGN>(a);
-    fft_reg<16, SIGN>(b);
-}
-
 }  // namespace fcw
