@@ -1034,6 +1034,13 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) tx_kernel(const KP
                                     n + 1 < n1 ? in_u + (long long)(n + 1) * P.row_len : nullptr, n > nfirst,
                                     spec0, spec1, S.scr, S.stw);
             team_sync<G>(g, TT);
+            // bins no subband touches are zeroed in the same phase as the first
+            // rank of secondary contributions (disjoint bins: one barrier less)
+            for (int k = gtid; k < P.n_zero; k += TT) {
+                const int q = __ldg(&P.zero_list[k]);
+                spec0[q] = zero2();
+                spec1[q] = zero2();
+            }
             // secondary contributions of shared transition bins, in rank order
             for (int l = 0; l < P.n_lvl; ++l) {
                 for (int k = P.lvl_start[l] + gtid; k < P.lvl_start[l + 1]; k += TT) {
@@ -1043,12 +1050,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) tx_kernel(const KP
                 }
                 team_sync<G>(g, TT);
             }
-            for (int k = gtid; k < P.n_zero; k += TT) {
-                const int q = __ldg(&P.zero_list[k]);
-                spec0[q] = zero2();
-                spec1[q] = zero2();
-            }
-            team_sync<G>(g, TT);
+            if (P.n_lvl == 0) team_sync<G>(g, TT);
 
             float2 cr[8];
 #pragma unroll
@@ -1070,7 +1072,9 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) tx_kernel(const KP
                     team_fft<N, T, kPPT, +1, 2, true, long_twl<N>()>(v, bufs, long_twl<N>() ? S.ltw : P.tw, 1, gtid, act,
                                                                     G == 1 ? 0 : 1 + g, TT);
             }
-            team_sync<G>(g, TT);  // every thread has read its carry before it is overwritten
+            // every thread has read its carry before it is overwritten: the long
+            // transform's exchange barriers already order that for N >= 512
+            if (N < 512 || (P.dbg_skip & 2)) team_sync<G>(g, TT);
             // symbol-wise overlap-add: block 0 at 0, block 1 at N/2, carry from n-1
             if (act) {
                 const bool emit = n >= n0;
