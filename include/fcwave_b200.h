@@ -166,6 +166,14 @@ int fcw_awgn(const fcw_plan* plan, void* wave, int64_t wave_unit_stride, int64_t
 int fcw_wave_power(const fcw_plan* plan, const void* wave, int64_t wave_unit_stride, int64_t wave_len, int S,
                    int64_t begin, int64_t end, double* power, void* stream);
 
+/* Welch PSD (metrics.cpp:128-155, row f4) of S device waveforms of wave_len
+ * samples: Hann windows of seg_len (a power of two in [64, 4096]) hopping
+ * lround(seg_len (1 - overlap_frac)), |FFT|^2 averaged and scaled by
+ * 1 / (n_seg sum w^2).  Per-bin sums in double, deterministic order.
+ * Blocking: psd[S][seg_len] (double) on the host. */
+int fcw_psd(const void* wave, int64_t wave_unit_stride, int64_t wave_len, int S, int seg_len, double overlap_frac,
+            double* psd, void* stream);
+
 /* ------------------------------------ continuous FC filterbank (row f2) */
 
 /* Replaces tx_continuous / rx_continuous (fc_core.hpp:64-77, fc_core.cpp:

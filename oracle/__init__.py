@@ -112,6 +112,7 @@ def lib():
         L.fco_awgn.restype = None
         L.fco_measure_power.argtypes = [_f64p, C.c_int64, C.c_int64, C.c_int64]
         L.fco_measure_power.restype = C.c_double
+        L.fco_psd.argtypes = [_f64p, C.c_int64, C.c_int, C.c_double, _f64p]
         L.fco_tx_continuous.argtypes = [C.c_int, C.c_double, C.c_int, _i32p, _i32p, _f64p, _f64p, _i64p, C.c_int,
                                         _f64p, C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
         L.fco_rx_continuous.argtypes = [_f64p, C.c_int64, C.c_int, C.c_double, C.c_int, C.c_int, _f64p, _f64p,
@@ -154,6 +155,7 @@ def ref():
         R.fcwref_awgn_with_variance.argtypes = [_f64p, C.c_longlong, C.c_double, C.c_ulonglong]
         R.fcwref_measure_power.argtypes = [_f64p, C.c_longlong, C.c_longlong, C.c_longlong, C.POINTER(C.c_double)]
         _i64p = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
+        R.fcwref_psd.argtypes = [_f64p, C.c_longlong, C.c_int, C.c_double, _f64p]
         R.fcwref_tx_continuous.argtypes = [C.c_int, C.c_double, C.c_int, _i32p, _i32p, _f64p, _f64p, _i64p,
                                            C.c_int, _f64p, C.c_longlong, C.POINTER(C.c_longlong),
                                            C.POINTER(C.c_longlong)]
@@ -389,6 +391,14 @@ def measure_power(wave, begin: int, end: int) -> float:
     return float(lib().fco_measure_power(w.view(np.float64), len(w), begin, end))
 
 
+def psd(x, seg_len: int, overlap_frac: float = 0.5) -> np.ndarray:
+    """metrics.cpp:128-155 Welch PSD."""
+    w = _as_f64(x)
+    out = np.zeros(seg_len, np.float64)
+    _check(lib().fco_psd(w, len(w) // 2, seg_len, overlap_frac, out), "psd")
+    return out
+
+
 def _cont_cap(N, Ls, lens):
     return int(max((ln + L) // (L // 2) + 3 for L, ln in zip(Ls, lens)) * (N // 2) + 2 * N)
 
@@ -562,3 +572,10 @@ class Ref:
         _check(ref().fcwref_rx_continuous(w, n, N, overlap, L, c, np.asarray(window, np.float64), out, cap,
                                           C.byref(no)), "ref rx_continuous", ref())
         return out.view(np.complex128)[: no.value].copy()
+
+    @staticmethod
+    def psd(x, seg_len: int, overlap_frac: float = 0.5) -> np.ndarray:
+        w = _as_f64(x)
+        out = np.zeros(seg_len, np.float64)
+        _check(ref().fcwref_psd(w, len(w) // 2, seg_len, overlap_frac, out), "ref psd", ref())
+        return out

@@ -675,3 +675,38 @@ int fco_rx_continuous(const double* wave, int64_t len, int N, double overlap, in
     free(z);
     return 0;
 }
+
+/* ------------------------------------------------------ Welch PSD (row f4) */
+
+/* metrics.cpp:128-155 (psd): Hann-windowed segments of seg_len hopping
+ * lround(seg_len (1 - overlap)), |FFT|^2 accumulated, scaled by
+ * 1 / (n_seg sum win^2).  Returns 1 for the reference's invalid_argument. */
+int fco_psd(const double* x, int64_t len, int seg_len, double overlap_frac, double* out) {
+    if (seg_len <= 0 || seg_len > len) return 1;
+    if (overlap_frac < 0.0 || overlap_frac >= 1.0) return 1;
+    long hop = lround(seg_len * (1.0 - overlap_frac));
+    if (hop < 1) hop = 1;
+    double* win = (double*)malloc(sizeof(double) * (size_t)seg_len);
+    double wpow = 0.0;
+    for (int i = 0; i < seg_len; ++i) {
+        win[i] = 0.5 - 0.5 * cos(2.0 * kPi * i / seg_len);
+        wpow += win[i] * win[i];
+    }
+    double* seg = zalloc((size_t)seg_len);
+    for (int i = 0; i < seg_len; ++i) out[i] = 0.0;
+    int n_seg = 0;
+    for (int64_t start = 0; start + seg_len <= len; start += hop) {
+        for (int i = 0; i < seg_len; ++i) {
+            seg[2 * i] = x[2 * (start + i)] * win[i];
+            seg[2 * i + 1] = x[2 * (start + i) + 1] * win[i];
+        }
+        fco_fft(seg, seg_len, 0);
+        for (int i = 0; i < seg_len; ++i) out[i] += seg[2 * i] * seg[2 * i] + seg[2 * i + 1] * seg[2 * i + 1];
+        ++n_seg;
+    }
+    const double scale = 1.0 / ((double)n_seg * wpow);
+    for (int i = 0; i < seg_len; ++i) out[i] *= scale;
+    free(win);
+    free(seg);
+    return 0;
+}

@@ -84,6 +84,9 @@ void fco_gauss_complex(uint64_t* state, double* re, double* im);
 void fco_awgn(double* wave, int64_t len, double sigma2, uint64_t seed);
 double fco_measure_power(const double* wave, int64_t len, int64_t begin, int64_t end);
 
+/* Welch PSD (f4): metrics.cpp:128-155. */
+int fco_psd(const double* x, int64_t len, int seg_len, double overlap_frac, double* out);
+
 /* Continuous FC filterbank (f2): fc_core.cpp:155-223. */
 int fco_continuous_block_count(int stream_len, const fco_params* p);
 int fco_tx_continuous(int N, double overlap, int M, const int* Ls, const int* cs, const double* windows,

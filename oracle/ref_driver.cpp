@@ -350,4 +350,12 @@ int fcwref_rx_continuous(const double* wave, long long len, int N, double overla
     });
 }
 
+/* ---- Welch PSD (f4): metrics.hpp:75 ---- */
+int fcwref_psd(const double* x, long long len, int seg_len, double overlap_frac, double* out) {
+    return guarded([&] {
+        const std::vector<double> p = fcwave::psd(to_cvec(x, (std::size_t)len), seg_len, overlap_frac);
+        std::copy(p.begin(), p.end(), out);
+    });
+}
+
 }  // extern "C"

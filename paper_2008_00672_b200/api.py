@@ -555,6 +555,15 @@ class LinkStats:
         return float(np.sum(self.bit_errors)) / float(np.sum(self.n_bits))
 
 
+def psd(wave, wave_len: int, S: int, seg_len: int, overlap_frac: float = 0.5, stream=None,
+        wave_stride: int = 0) -> np.ndarray:
+    """Welch PSD (metrics.cpp:128-155) of S device waveforms -> [S][seg_len]."""
+    out = np.zeros((max(S, 1), seg_len), np.float64)
+    check(lib().fcw_psd(_dev_ptr(wave), wave_stride, wave_len, S, seg_len, overlap_frac,
+                        out.ctypes.data_as(C.POINTER(C.c_double)), _stream_ptr(stream)))
+    return out[:S]
+
+
 def evm_db_from_sums(num: float, den: float) -> float:
     """metrics.cpp:115-127 (evm_db) from accumulated sums: -10 log10(num/den),
     300 dB cap; zero reference power is an error."""

@@ -694,6 +694,24 @@ int fcw_wave_power(const fcw_plan* p, const void* wave, int64_t wave_stride, int
     return FCW_OK;
 }
 
+int fcw_psd(const void* wave, int64_t wave_stride, int64_t wave_len, int S, int seg_len, double overlap,
+            double* out, void* stream) {
+    if (!wave || !out) return fail(FCW_EINVAL, "null argument");
+    if (seg_len <= 0 || seg_len > wave_len) return fail(FCW_EINVAL, "waveform shorter than one segment");
+    if (overlap < 0.0 || overlap >= 1.0) return fail(FCW_EINVAL, "overlap fraction in [0,1)");  // metrics.cpp:131
+    if (!is_pow2(seg_len) || seg_len < 64 || seg_len > 4096)
+        return fail(FCW_ENOTSUP, "seg_len must be a power of two in [64, 4096]");
+    if (S < 0) return fail(FCW_EINVAL, "negative unit count");
+    if (wave_stride == 0) wave_stride = wave_len;
+    if (wave_stride < wave_len) return fail(FCW_EINVAL, "waveform unit stride smaller than its length");
+    if (S == 0) return FCW_OK;
+    if (S > 65535) return fail(FCW_ENOTSUP, "at most 65535 units per call");
+    const cudaError_t e = fcw::psd(static_cast<const float2*>(wave), wave_stride, wave_len, S, seg_len, overlap, out,
+                                   static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "psd");
+    return FCW_OK;
+}
+
 // ------------------------------------------------------ host-buffer pipeline
 
 namespace {

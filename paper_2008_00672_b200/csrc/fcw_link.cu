@@ -13,8 +13,11 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdint>
+#include <vector>
 
+#include "fcw_fft.cuh"
 #include "fcw_internal.hpp"
 
 namespace fcw {
@@ -183,6 +186,89 @@ cudaError_t reduce_to_host(int S, int chunks, cudaStream_t st, Launch&& launch, 
     return e;
 }
 
+// ---------------------------------------------------------- Welch PSD (f4)
+// metrics.cpp:128-155: Hann-windowed segments, |FFT_L|^2 summed per bin.
+// Grid (chunks, S): a CTA sums |X|^2 of segments [c*spc, (c+1)*spc) of unit u
+// in double, in segment order per thread; warps (L <= 256: one segment per
+// warp) or the whole CTA (L >= 512: T = L/16 threads x 16 points) transform;
+// per-CTA partials are summed in chunk order by psd_reduce_kernel.
+constexpr int kPsdSegPerCta = 32;
+
+template <int L>
+__global__ void __launch_bounds__(256) psd_kernel(const float2* __restrict__ wave, long long stride,
+                                                  const float* __restrict__ win, int hop, int n_seg,
+                                                  const float2* __restrict__ tw, int ts, double* __restrict__ part) {
+    extern __shared__ float2 psd_smem[];
+    const long long u = blockIdx.y;
+    const float2* w = wave + u * stride;
+    const int s0 = blockIdx.x * kPsdSegPerCta, s1 = min(n_seg, s0 + kPsdSegPerCta);
+    double* dst = part + ((long long)u * gridDim.x + blockIdx.x) * L;
+    if constexpr (L <= 256) {
+        constexpr int PPT = L / 32;
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        float2* const bufs[1] = {psd_smem + warp * (L + L / 16 + 2)};
+        double acc[PPT];
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) acc[k] = 0.0;
+        for (int sg = s0 + warp; sg < s1; sg += 8) {
+            const float2* x = w + (long long)sg * hop;
+            float2 v[1][PPT];
+#pragma unroll
+            for (int k = 0; k < PPT; ++k) v[0][k] = cscale(x[lane + 32 * k], win[lane + 32 * k]);
+            team_fft<L, 32, PPT, -1, 1, false>(v, bufs, tw, ts, lane, true);
+#pragma unroll
+            for (int k = 0; k < PPT; ++k) acc[k] += (double)v[0][k].x * v[0][k].x + (double)v[0][k].y * v[0][k].y;
+            __syncwarp();
+        }
+        // fixed-order sum over the 8 warps
+        __shared__ double red[256 * 8];
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) red[warp * L + lane + 32 * k] = acc[k];
+        __syncthreads();
+        for (int b = threadIdx.x; b < L; b += 256) {
+            double t = 0.0;
+            for (int q = 0; q < 8; ++q) t += red[q * L + b];
+            dst[b] = t;
+        }
+    } else {
+        constexpr int T = L / 16;
+        float2* const bufs[1] = {psd_smem};
+        const int t = threadIdx.x;
+        const bool act = t < T;
+        double acc[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) acc[k] = 0.0;
+        for (int sg = s0; sg < s1; ++sg) {
+            const float2* x = w + (long long)sg * hop;
+            float2 v[1][16];
+            if (act) {
+#pragma unroll
+                for (int k = 0; k < 16; ++k) v[0][k] = cscale(x[t + T * k], win[t + T * k]);
+            }
+            team_fft<L, T, 16, -1, 1, true>(v, bufs, tw, ts, t, act);
+            if (act) {
+#pragma unroll
+                for (int k = 0; k < 16; ++k) acc[k] += (double)v[0][k].x * v[0][k].x + (double)v[0][k].y * v[0][k].y;
+            }
+            __syncthreads();
+        }
+        if (act) {
+#pragma unroll
+            for (int k = 0; k < 16; ++k) dst[t + T * k] = acc[k];
+        }
+    }
+}
+
+__global__ void psd_reduce_kernel(const double* __restrict__ part, int chunks, int L, int S, double scale,
+                                  double* __restrict__ out) {
+    const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (idx >= (long long)S * L) return;
+    const long long u = idx / L, b = idx - u * L;
+    double t = 0.0;
+    for (int c = 0; c < chunks; ++c) t += part[(u * chunks + c) * L + b];
+    out[idx] = t * scale;
+}
+
 }  // namespace
 
 cudaError_t link_stats(const Plan& p, const float2* grid, long long stride, int S, uint64_t seed, long long unit0,
@@ -227,6 +313,69 @@ cudaError_t wave_power(const float2* wave, long long stride, int S, long long be
     if (e == cudaSuccess)
         for (int u = 0; u < S; ++u) power[u] = host[u].a / (double)(end - begin);
     delete[] host;
+    return e;
+}
+
+cudaError_t psd(const float2* wave, long long stride, long long len, int S, int L, double overlap, double* out_host,
+                cudaStream_t st) {
+    long hop = std::lround(L * (1.0 - overlap));
+    if (hop < 1) hop = 1;
+    const int n_seg = (int)((len - L) / hop + 1);
+    const int chunks = (n_seg + kPsdSegPerCta - 1) / kPsdSegPerCta;
+    std::vector<float> win(L);
+    std::vector<float2> tw(L);
+    double wpow = 0.0;
+    for (int i = 0; i < L; ++i) {
+        const double v = 0.5 - 0.5 * std::cos(2.0 * 3.14159265358979323846 * i / L);
+        win[i] = (float)v;
+        wpow += v * v;
+        const double a = -2.0 * 3.14159265358979323846 * i / L;
+        tw[i] = make_float2((float)std::cos(a), (float)std::sin(a));
+    }
+    char* scratch = nullptr;
+    const size_t part_b = sizeof(double) * (size_t)S * chunks * L, out_b = sizeof(double) * (size_t)S * L;
+    const size_t tab_b = (sizeof(float) + sizeof(float2)) * L;
+    cudaError_t e = scratch_alloc(&scratch, part_b + out_b + tab_b, st);
+    if (e != cudaSuccess) return e;
+    double* part = reinterpret_cast<double*>(scratch);
+    double* dout = reinterpret_cast<double*>(scratch + part_b);
+    float2* d_tw = reinterpret_cast<float2*>(scratch + part_b + out_b);
+    float* d_win = reinterpret_cast<float*>(scratch + part_b + out_b + sizeof(float2) * L);
+    e = cudaMemcpyAsync(d_win, win.data(), sizeof(float) * L, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_tw, tw.data(), sizeof(float2) * L, cudaMemcpyHostToDevice, st);
+    const dim3 grid(chunks, S);
+#define FCW_PSD_CASE(LL)                                                                                       \
+    case LL: {                                                                                                 \
+        const size_t smem = (LL <= 256 ? 8 : 1) * (size_t)(LL + LL / 16 + 2) * sizeof(float2);                 \
+        if (smem > 48 * 1024) cudaFuncSetAttribute(psd_kernel<LL>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                                   (int)smem);                                                 \
+        psd_kernel<LL><<<grid, 256, smem, st>>>(wave, stride, d_win, (int)hop, n_seg, d_tw, 1, part);          \
+        break;                                                                                                 \
+    }
+    if (e == cudaSuccess) {
+        switch (L) {
+            FCW_PSD_CASE(64)
+            FCW_PSD_CASE(128)
+            FCW_PSD_CASE(256)
+            FCW_PSD_CASE(512)
+            FCW_PSD_CASE(1024)
+            FCW_PSD_CASE(2048)
+            FCW_PSD_CASE(4096)
+            default: e = cudaErrorInvalidValue;
+        }
+#undef FCW_PSD_CASE
+        if (e == cudaSuccess) e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) {
+        const long long n = (long long)S * L;
+        psd_reduce_kernel<<<(int)((n + 255) / 256), 256, 0, st>>>(part, chunks, L, S, 1.0 / ((double)n_seg * wpow),
+                                                                 dout);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(out_host, dout, out_b, cudaMemcpyDeviceToHost, st);
+    const cudaError_t f = cudaFreeAsync(scratch, st);
+    if (e == cudaSuccess) e = f;
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     return e;
 }
 

@@ -101,3 +101,34 @@ def test_noisy_link_ber_matches_oracle(snr_db):
     assert st.bit_errors.sum() > 0 if snr_db < 8 else True
     # EVM tracks the SNR (flat AWGN): within a dB of it
     assert abs(st.evm_db() - snr_db) < 1.0
+
+
+@pytest.mark.parametrize("seg", [64, 256, 1024, 4096])
+def test_psd_matches_oracle(seg):
+    """Welch PSD (metrics.cpp:128-155) of device waveforms vs the oracle."""
+    w = configs.config5()
+    plan = w.plan()
+    S = 2
+    grid = torch.empty((S, w.B, plan.row_active), dtype=torch.complex64, device="cuda")
+    plan.gen_qam(3, 0, S, w.bits_per_symbol, grid)
+    wave = torch.empty((S, plan.Q), dtype=torch.complex64, device="cuda")
+    plan.tx(grid, wave, S)
+    n = 40 * seg + 5
+    got = api.psd(wave, n, S, seg, 0.5, wave_stride=plan.Q)
+    x = wave.cpu().numpy()
+    for u in range(S):
+        want = O.psd(x[u, :n].astype(np.complex128), seg, 0.5)
+        assert np.max(np.abs(got[u] - want)) <= 1e-5 * np.max(want)
+        assert rel_rms(got[u], want) <= 1e-5
+
+
+def test_psd_tone_and_errors():
+    seg = 64
+    t = np.arange(seg * 40)
+    d = _dev(np.exp(2j * np.pi * 12 * t / seg).astype(np.complex64)[None])
+    p = api.psd(d, len(t), 1, seg)[0]
+    assert int(np.argmax(p)) == 12 and p[12] / p[20] > 1e6
+    with pytest.raises(ValueError):
+        api.psd(d, 16, 1, 64)  # waveform shorter than one segment (metrics.cpp:129-130)
+    with pytest.raises(ValueError):
+        api.psd(d, len(t), 1, 64, 1.0)

@@ -88,3 +88,24 @@ def test_evm_db_edges():
     assert api.evm_db_from_sums(0.01, 1.0) == pytest.approx(20.0)
     with pytest.raises(ValueError):
         api.evm_db_from_sums(1.0, 0.0)
+
+
+# ---------------------------------------------------------------- f4 Welch PSD
+@needs_ref
+@pytest.mark.parametrize("seg,ov", [(64, 0.5), (1024, 0.5), (256, 0.0), (128, 0.75), (4096, 0.5)])
+def test_psd_matches_reference(seg, ov):
+    rng = np.random.default_rng(seg)
+    x = rng.standard_normal(3 * seg + 17) + 1j * rng.standard_normal(3 * seg + 17)
+    assert np.array_equal(O.psd(x, seg, ov), O.Ref.psd(x, seg, ov))
+
+
+def test_psd_known_answers():  # proj/tests/test_metrics.cpp:132-156
+    seg = 64
+    t = np.arange(seg * 40)
+    p = O.psd(np.exp(2j * np.pi * 12 * t / seg), seg)
+    assert int(np.argmax(p)) == 12 and p[12] / (p[20] + 1e-300) > 1e6
+    n = O.awgn(np.zeros(seg * 150, complex), 1.0, 3)  # GaussianRng(3).next_complex() stream
+    pn = O.psd(n, seg)
+    assert np.all(np.abs(10 * np.log10(pn / pn.mean())) < 1.0)
+    with pytest.raises(ValueError):  # std::invalid_argument
+        O.psd(np.zeros(16, complex), 64)
