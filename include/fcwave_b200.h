@@ -161,6 +161,19 @@ int fcw_link_stats(const fcw_plan* plan, const void* grid, int64_t grid_unit_str
 int fcw_awgn(const fcw_plan* plan, void* wave, int64_t wave_unit_stride, int64_t wave_len, int S, double sigma2,
              uint64_t seed, int64_t unit0, void* stream);
 
+/* draw_tdl (channel.cpp:101-111), host: delays[k] = lround(delay_ns[k] 1e-9 fs),
+ * gains[k] = sqrt(power_lin[k]) * GaussianRng(seed).next_complex() (complex
+ * as interleaved doubles, 2 n_taps). */
+int fcw_draw_tdl(const double* delay_ns, const double* power_lin, int n_taps, double fs_hz, uint64_t seed,
+                 int* delays, double* gains);
+
+/* apply_channel (channel.cpp:113-124) on S device waveforms, out of place:
+ * out[u][t] = sum_k g[u][k] in[u][t - d[u][k]] (t >= d[u][k]).  delays
+ * [S][n_taps] and gains [S][n_taps] (interleaved complex doubles) are host
+ * arrays, one tap line per unit, n_taps <= 64.  Blocking. */
+int fcw_apply_channel(const void* wave_in, void* wave_out, int64_t wave_unit_stride, int64_t wave_len, int S,
+                      const int* delays, const double* gains, int n_taps, void* stream);
+
 /* measure_power (channel.cpp:148-155) per unit: mean |v|^2 over
  * [begin, end) clipped to [0, wave_len).  Blocking: power[S] on the host. */
 int fcw_wave_power(const fcw_plan* plan, const void* wave, int64_t wave_unit_stride, int64_t wave_len, int S,

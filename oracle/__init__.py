@@ -112,6 +112,10 @@ def lib():
         L.fco_awgn.restype = None
         L.fco_measure_power.argtypes = [_f64p, C.c_int64, C.c_int64, C.c_int64]
         L.fco_measure_power.restype = C.c_double
+        L.fco_draw_tdl.argtypes = [_f64p, _f64p, C.c_int, C.c_double, C.c_uint64, _i32p, _f64p]
+        L.fco_draw_tdl.restype = None
+        L.fco_apply_channel.argtypes = [_f64p, C.c_int64, _i32p, _f64p, C.c_int, _f64p]
+        L.fco_apply_channel.restype = None
         L.fco_psd.argtypes = [_f64p, C.c_int64, C.c_int, C.c_double, _f64p]
         L.fco_tx_continuous.argtypes = [C.c_int, C.c_double, C.c_int, _i32p, _i32p, _f64p, _f64p, _i64p, C.c_int,
                                         _f64p, C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
@@ -155,6 +159,8 @@ def ref():
         R.fcwref_awgn_with_variance.argtypes = [_f64p, C.c_longlong, C.c_double, C.c_ulonglong]
         R.fcwref_measure_power.argtypes = [_f64p, C.c_longlong, C.c_longlong, C.c_longlong, C.POINTER(C.c_double)]
         _i64p = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
+        R.fcwref_draw_tdl.argtypes = [_f64p, _f64p, C.c_int, C.c_double, C.c_ulonglong, _i32p, _f64p]
+        R.fcwref_apply_channel.argtypes = [_f64p, C.c_longlong, _i32p, _f64p, C.c_int]
         R.fcwref_psd.argtypes = [_f64p, C.c_longlong, C.c_int, C.c_double, _f64p]
         R.fcwref_tx_continuous.argtypes = [C.c_int, C.c_double, C.c_int, _i32p, _i32p, _f64p, _f64p, _i64p,
                                            C.c_int, _f64p, C.c_longlong, C.POINTER(C.c_longlong),
@@ -391,6 +397,24 @@ def measure_power(wave, begin: int, end: int) -> float:
     return float(lib().fco_measure_power(w.view(np.float64), len(w), begin, end))
 
 
+def draw_tdl(delay_ns, power_lin, fs_hz: float, seed: int):
+    """channel.cpp:101-111 -> (delays int32, gains complex128)."""
+    d = np.ascontiguousarray(delay_ns, np.float64)
+    p = np.ascontiguousarray(power_lin, np.float64)
+    dl = np.zeros(len(d), np.int32)
+    g = np.zeros(2 * len(d), np.float64)
+    lib().fco_draw_tdl(d, p, len(d), fs_hz, seed, dl, g)
+    return dl, g.view(np.complex128)
+
+
+def apply_channel(wave, delays, gains) -> np.ndarray:
+    """channel.cpp:113-124."""
+    w = _as_f64(wave)
+    out = np.zeros_like(w)
+    lib().fco_apply_channel(w, len(w) // 2, _i32(delays), _as_f64(gains), len(delays), out)
+    return out.view(np.complex128)
+
+
 def psd(x, seg_len: int, overlap_frac: float = 0.5) -> np.ndarray:
     """metrics.cpp:128-155 Welch PSD."""
     w = _as_f64(x)
@@ -579,3 +603,19 @@ class Ref:
         out = np.zeros(seg_len, np.float64)
         _check(ref().fcwref_psd(w, len(w) // 2, seg_len, overlap_frac, out), "ref psd", ref())
         return out
+
+    @staticmethod
+    def draw_tdl(delay_ns, power_lin, fs_hz: float, seed: int):
+        d = np.ascontiguousarray(delay_ns, np.float64)
+        p = np.ascontiguousarray(power_lin, np.float64)
+        dl = np.zeros(len(d), np.int32)
+        g = np.zeros(2 * len(d), np.float64)
+        _check(ref().fcwref_draw_tdl(d, p, len(d), fs_hz, seed, dl, g), "ref draw_tdl", ref())
+        return dl, g.view(np.complex128)
+
+    @staticmethod
+    def apply_channel(wave, delays, gains) -> np.ndarray:
+        w = _c128(wave).copy()
+        _check(ref().fcwref_apply_channel(w.view(np.float64), len(w), _i32(delays), _as_f64(gains), len(delays)),
+               "ref apply_channel", ref())
+        return w

@@ -710,3 +710,36 @@ int fco_psd(const double* x, int64_t len, int seg_len, double overlap_frac, doub
     free(seg);
     return 0;
 }
+
+/* ---------------------------------------------------- TDL channel (row f3) */
+
+/* channel.cpp:101-111 draw_tdl: delays lround(delay_ns 1e-9 fs), gains
+ * sqrt(power) * GaussianRng(seed).next_complex() per tap in order. */
+void fco_draw_tdl(const double* delay_ns, const double* power_lin, int n_taps, double fs_hz, uint64_t seed,
+                  int* delays, double* gains) {
+    uint64_t st = seed ? seed : 0x1234567890abcdefULL;
+    for (int k = 0; k < n_taps; ++k) {
+        delays[k] = (int)lround(delay_ns[k] * 1e-9 * fs_hz);
+        double nr, ni;
+        fco_gauss_complex(&st, &nr, &ni);
+        const double a = sqrt(power_lin[k]);
+        gains[2 * k] = a * nr;
+        gains[2 * k + 1] = a * ni;
+    }
+}
+
+/* channel.cpp:113-124 apply_channel: out[t] = sum_k g_k w[t - d_k] (t >= d_k),
+ * taps accumulated in tap order. */
+void fco_apply_channel(const double* w, int64_t len, const int* delays, const double* gains, int n_taps,
+                       double* out) {
+    for (int64_t t = 0; t < 2 * len; ++t) out[t] = 0.0;
+    for (int k = 0; k < n_taps; ++k) {
+        const int64_t d = delays[k];
+        const double gr = gains[2 * k], gi = gains[2 * k + 1];
+        for (int64_t t = d; t < len; ++t) {
+            const double xr = w[2 * (t - d)], xi = w[2 * (t - d) + 1];
+            out[2 * t] += gr * xr - gi * xi;
+            out[2 * t + 1] += gr * xi + gi * xr;
+        }
+    }
+}

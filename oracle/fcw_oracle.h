@@ -84,6 +84,12 @@ void fco_gauss_complex(uint64_t* state, double* re, double* im);
 void fco_awgn(double* wave, int64_t len, double sigma2, uint64_t seed);
 double fco_measure_power(const double* wave, int64_t len, int64_t begin, int64_t end);
 
+/* TDL channel (f3): channel.cpp:101-124. */
+void fco_draw_tdl(const double* delay_ns, const double* power_lin, int n_taps, double fs_hz, uint64_t seed,
+                  int* delays, double* gains);
+void fco_apply_channel(const double* w, int64_t len, const int* delays, const double* gains, int n_taps,
+                       double* out);
+
 /* Welch PSD (f4): metrics.cpp:128-155. */
 int fco_psd(const double* x, int64_t len, int seg_len, double overlap_frac, double* out);
 

@@ -358,4 +358,28 @@ int fcwref_psd(const double* x, long long len, int seg_len, double overlap_frac,
     });
 }
 
+/* ---- TDL channel (f3): channel.hpp:34-60 ---- */
+int fcwref_draw_tdl(const double* delay_ns, const double* power_lin, int n_taps, double fs_hz,
+                    unsigned long long seed, int* delays, double* gains) {
+    return guarded([&] {
+        fcwave::TdlProfile p;
+        for (int k = 0; k < n_taps; ++k) p.taps.push_back({delay_ns[k], power_lin[k]});
+        const fcwave::ChannelRealization ch = fcwave::draw_tdl(p, fs_hz, seed);
+        for (int k = 0; k < n_taps; ++k) delays[k] = ch.delays_samples[k];
+        from_cvec(ch.gains, gains);
+    });
+}
+
+int fcwref_apply_channel(double* wave, long long len, const int* delays, const double* gains, int n_taps) {
+    return guarded([&] {
+        fcwave::Waveform w;
+        w.samples = to_cvec(wave, (std::size_t)len);
+        fcwave::ChannelRealization ch;
+        ch.delays_samples.assign(delays, delays + n_taps);
+        ch.gains = to_cvec(gains, (std::size_t)n_taps);
+        fcwave::apply_channel(w, ch);
+        from_cvec(w.samples, wave);
+    });
+}
+
 }  // extern "C"

@@ -555,6 +555,50 @@ class LinkStats:
         return float(np.sum(self.bit_errors)) / float(np.sum(self.n_bits))
 
 
+@dataclass
+class ChannelRealization:  # channel.hpp:48-54
+    delays_samples: np.ndarray
+    gains: np.ndarray
+
+    def frequency_response(self, n_fft: int) -> np.ndarray:
+        """channel.cpp:91-98: DFT of the tap line on the n_fft grid."""
+        h = np.zeros(n_fft, np.complex128)
+        for d, g in zip(self.delays_samples, self.gains):
+            h[int(d) % n_fft] += g
+        return np.fft.fft(h)
+
+
+def exponential_profile(rms_ds_ns: float, step_ns: float, n_taps: int) -> tuple[np.ndarray, np.ndarray]:
+    """TdlProfile::exponential (channel.cpp:75-89): (delay_ns, power_lin)."""
+    if rms_ds_ns <= 0.0 or step_ns <= 0.0 or n_taps < 1:
+        raise ValueError("invalid exponential profile parameters")
+    d = np.arange(n_taps) * step_ns
+    p = np.exp(-d / rms_ds_ns)
+    return d, p / p.sum()
+
+
+def draw_tdl(delay_ns, power_lin, fs_hz: float, seed: int) -> ChannelRealization:
+    """draw_tdl (channel.cpp:101-111) through the C ABI."""
+    d = np.ascontiguousarray(delay_ns, np.float64)
+    p = np.ascontiguousarray(power_lin, np.float64)
+    dl = np.zeros(len(d), np.int32)
+    g = np.zeros(2 * len(d), np.float64)
+    check(lib().fcw_draw_tdl(d.ctypes.data, p.ctypes.data, len(d), fs_hz, seed, dl.ctypes.data, g.ctypes.data))
+    return ChannelRealization(dl, g.view(np.complex128))
+
+
+def apply_channel(wave_in, wave_out, wave_len: int, S: int, channels: Sequence[ChannelRealization], stream=None,
+                  wave_stride: int = 0) -> None:
+    """apply_channel (channel.cpp:113-124) on S device waveforms, one tap line per unit."""
+    n = len(channels[0].gains) if channels else 0
+    if any(len(c.gains) != n for c in channels) or len(channels) != S:
+        raise ValueError("one channel realization per unit, equal tap counts")
+    d = np.ascontiguousarray(np.concatenate([c.delays_samples for c in channels]) if S else np.zeros(0), np.int32)
+    g = np.ascontiguousarray(np.concatenate([c.gains for c in channels]) if S else np.zeros(0), np.complex128)
+    check(lib().fcw_apply_channel(_dev_ptr(wave_in), _dev_ptr(wave_out), wave_stride, wave_len, S, d.ctypes.data,
+                                  g.ctypes.data, n, _stream_ptr(stream)))
+
+
 def psd(wave, wave_len: int, S: int, seg_len: int, overlap_frac: float = 0.5, stream=None,
         wave_stride: int = 0) -> np.ndarray:
     """Welch PSD (metrics.cpp:128-155) of S device waveforms -> [S][seg_len]."""

@@ -694,6 +694,48 @@ int fcw_wave_power(const fcw_plan* p, const void* wave, int64_t wave_stride, int
     return FCW_OK;
 }
 
+int fcw_draw_tdl(const double* delay_ns, const double* power_lin, int n_taps, double fs_hz, uint64_t seed,
+                 int* delays, double* gains) {
+    if (n_taps < 0 || (n_taps > 0 && (!delay_ns || !power_lin || !delays || !gains)))
+        return fail(FCW_EINVAL, "null argument");
+    uint64_t st = seed ? seed : 0x1234567890abcdefULL;  // GaussianRng ctor (channel.cpp:26)
+    auto next = [&]() {
+        uint64_t z = (st += 0x9e3779b97f4a7c15ULL);
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+        return z ^ (z >> 31);
+    };
+    for (int k = 0; k < n_taps; ++k) {
+        delays[k] = (int)std::lround(delay_ns[k] * 1e-9 * fs_hz);
+        const double u1 = ((double)(next() >> 11) + 1.0) * 0x1p-53;
+        const double u2 = (double)(next() >> 11) * 0x1p-53;
+        const double r = std::sqrt(-std::log(u1)), a = std::sqrt(power_lin[k]);
+        gains[2 * k] = a * (r * std::cos(2.0 * 3.14159265358979323846 * u2));
+        gains[2 * k + 1] = a * (r * std::sin(2.0 * 3.14159265358979323846 * u2));
+    }
+    return FCW_OK;
+}
+
+int fcw_apply_channel(const void* in, void* out, int64_t stride, int64_t len, int S, const int* delays,
+                      const double* gains, int n_taps, void* stream) {
+    if (!in || !out || (n_taps > 0 && (!delays || !gains))) return fail(FCW_EINVAL, "null argument");
+    if (in == out) return fail(FCW_EINVAL, "apply_channel is out of place");
+    if (S < 0 || len < 0 || n_taps < 0) return fail(FCW_EINVAL, "negative size");
+    if (n_taps > 64) return fail(FCW_ENOTSUP, "at most 64 taps");
+    if (S > 65535) return fail(FCW_ENOTSUP, "at most 65535 units per call");
+    if (stride == 0) stride = len;
+    if (stride < len) return fail(FCW_EINVAL, "waveform unit stride smaller than its length");
+    if (S == 0 || len == 0) return FCW_OK;
+    for (long long i = 0; i < (long long)S * n_taps; ++i)
+        if (delays[i] < 0) return fail(FCW_EINVAL, "negative tap delay");
+    std::vector<float2> g((size_t)S * n_taps);
+    for (size_t i = 0; i < g.size(); ++i) g[i] = make_float2((float)gains[2 * i], (float)gains[2 * i + 1]);
+    const cudaError_t e = fcw::apply_channel(static_cast<const float2*>(in), static_cast<float2*>(out), stride, len, S,
+                                             delays, g.data(), n_taps, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "apply_channel");
+    return FCW_OK;
+}
+
 int fcw_psd(const void* wave, int64_t wave_stride, int64_t wave_len, int S, int seg_len, double overlap,
             double* out, void* stream) {
     if (!wave || !out) return fail(FCW_EINVAL, "null argument");

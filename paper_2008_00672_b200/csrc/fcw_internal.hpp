@@ -171,6 +171,8 @@ cudaError_t awgn(float2* wave, long long stride, long long len, int S, double si
                  long long unit0, cudaStream_t st);
 cudaError_t wave_power(const float2* wave, long long stride, int S, long long begin, long long end, double* power,
                        cudaStream_t st);
+cudaError_t apply_channel(const float2* in, float2* out, long long stride, long long len, int S, const int* delays,
+                          const float2* gains, int n_taps, cudaStream_t st);
 cudaError_t psd(const float2* wave, long long stride, long long len, int S, int L, double overlap, double* out_host,
                 cudaStream_t st);
 size_t rx_smem_bytes(const Plan& plan);

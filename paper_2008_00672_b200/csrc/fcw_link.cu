@@ -186,6 +186,37 @@ cudaError_t reduce_to_host(int S, int chunks, cudaStream_t st, Launch&& launch, 
     return e;
 }
 
+// ----------------------------------------------------- TDL channel (f3)
+// channel.cpp:113-124 apply_channel, per unit its own tap line:
+// out[t] = sum_k g_k in[t - d_k] over taps with d_k <= t, in tap order.
+constexpr int kMaxTaps = 64;
+__global__ void __launch_bounds__(256) channel_kernel(const float2* __restrict__ in, float2* __restrict__ out,
+                                                      long long stride, long long len, const int* __restrict__ delays,
+                                                      const float2* __restrict__ gains, int n_taps) {
+    __shared__ int sd[kMaxTaps];
+    __shared__ float2 sg[kMaxTaps];
+    const long long u = blockIdx.y;
+    for (int k = threadIdx.x; k < n_taps; k += blockDim.x) {
+        sd[k] = delays[u * n_taps + k];
+        sg[k] = gains[u * n_taps + k];
+    }
+    __syncthreads();
+    const float2* x = in + u * stride;
+    float2* y = out + u * stride;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < len; t += (long long)gridDim.x * blockDim.x) {
+        float2 acc = make_float2(0.f, 0.f);
+        for (int k = 0; k < n_taps; ++k) {
+            const long long j = t - sd[k];
+            if (j >= 0) {
+                const float2 v = __ldg(&x[j]);
+                acc.x = fmaf(sg[k].x, v.x, fmaf(-sg[k].y, v.y, acc.x));
+                acc.y = fmaf(sg[k].x, v.y, fmaf(sg[k].y, v.x, acc.y));
+            }
+        }
+        y[t] = acc;
+    }
+}
+
 // ---------------------------------------------------------- Welch PSD (f4)
 // metrics.cpp:128-155: Hann-windowed segments, |FFT_L|^2 summed per bin.
 // Grid (chunks, S): a CTA sums |X|^2 of segments [c*spc, (c+1)*spc) of unit u
@@ -376,6 +407,25 @@ cudaError_t psd(const float2* wave, long long stride, long long len, int S, int 
     const cudaError_t f = cudaFreeAsync(scratch, st);
     if (e == cudaSuccess) e = f;
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    return e;
+}
+
+cudaError_t apply_channel(const float2* in, float2* out, long long stride, long long len, int S, const int* delays,
+                          const float2* gains, int n_taps, cudaStream_t st) {
+    int* d = nullptr;
+    cudaError_t e = scratch_alloc(&d, (sizeof(int) + sizeof(float2)) * (size_t)S * n_taps, st);
+    if (e != cudaSuccess) return e;
+    float2* g = reinterpret_cast<float2*>(d + (size_t)S * n_taps);
+    e = cudaMemcpyAsync(d, delays, sizeof(int) * (size_t)S * n_taps, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(g, gains, sizeof(float2) * (size_t)S * n_taps, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) {
+        const int gx = (int)std::min<long long>((len + 255) / 256, 1184);
+        channel_kernel<<<dim3(gx, S), 256, 0, st>>>(in, out, stride, len, d, g, n_taps);
+        e = cudaGetLastError();
+    }
+    const cudaError_t f = cudaFreeAsync(d, st);
+    if (e == cudaSuccess) e = f;
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // host tap arrays may be released on return
     return e;
 }
 

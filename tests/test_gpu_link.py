@@ -132,3 +132,19 @@ def test_psd_tone_and_errors():
         api.psd(d, 16, 1, 64)  # waveform shorter than one segment (metrics.cpp:129-130)
     with pytest.raises(ValueError):
         api.psd(d, len(t), 1, 64, 1.0)
+
+
+def test_apply_channel_matches_oracle():
+    S, L = 3, 20000
+    d, p = api.exponential_profile(300.0, 20.0, 16)
+    chans = [api.draw_tdl(d, p, 122.88e6, O.derive_seed(4, u)) for u in range(S)]
+    rng = np.random.default_rng(6)
+    x = (rng.standard_normal((S, L)) + 1j * rng.standard_normal((S, L))).astype(np.complex64)
+    din, dout = _dev(x), torch.empty((S, L), dtype=torch.complex64, device="cuda")
+    api.apply_channel(din, dout, L, S, chans)
+    got = dout.cpu().numpy()
+    for u in range(S):
+        want = O.apply_channel(x[u].astype(np.complex128), chans[u].delays_samples, chans[u].gains)
+        assert rel_rms(got[u], want) <= 1e-6
+    with pytest.raises(ValueError):
+        api.apply_channel(din, din, L, S, chans)  # out of place only

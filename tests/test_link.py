@@ -109,3 +109,26 @@ def test_psd_known_answers():  # proj/tests/test_metrics.cpp:132-156
     assert np.all(np.abs(10 * np.log10(pn / pn.mean())) < 1.0)
     with pytest.raises(ValueError):  # std::invalid_argument
         O.psd(np.zeros(16, complex), 64)
+
+
+# -------------------------------------------------------------- f3 TDL channel
+@needs_ref
+def test_tdl_matches_reference():
+    from paper_2008_00672_b200 import api
+    d, p = api.exponential_profile(100.0, 10.0, 12)
+    for seed in (0, 5, O.derive_seed(9, 2)):
+        a = O.draw_tdl(d, p, 122.88e6, seed)
+        b = O.Ref.draw_tdl(d, p, 122.88e6, seed)
+        c = api.draw_tdl(d, p, 122.88e6, seed)  # the C ABI's host draw
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+        assert np.array_equal(c.delays_samples, b[0]) and np.array_equal(c.gains, b[1])
+    rng = np.random.default_rng(1)
+    x = rng.standard_normal(5000) + 1j * rng.standard_normal(5000)
+    assert np.array_equal(O.apply_channel(x, a[0], a[1]), O.Ref.apply_channel(x, a[0], a[1]))
+    # frequency response = DFT of the tap line (channel.cpp:91-98)
+    h = api.ChannelRealization(a[0], a[1]).frequency_response(64)
+    want = np.zeros(64, complex)
+    for dd, g in zip(a[0], a[1]):
+        want[dd % 64] += g
+    assert np.allclose(h, np.fft.fft(want))
+    assert abs(np.sum(p) - 1.0) < 1e-12
