@@ -331,6 +331,21 @@ int fcw_plan_create(fcw_plan** out, int N, double overlap, const int* cp_high, i
     }
     p->row_active = act_off;
     p->row_full = full_off;
+    // zero-bin kernel variant (tx_short_half / rx_short_half, ZV): uniform
+    // L = 256 at N = 4096 where every subband leaves DFT bins b with
+    // b / 16 in [5, 10] inactive and outside its window
+    p->zv = N == 4096 && M > 0;
+    for (int m = 0; m < M && p->zv; ++m) {
+        const fcw_subband& s = sbs[m];
+        if (s.L != 256) {
+            p->zv = false;
+            break;
+        }
+        for (int b = 80; b < 176 && p->zv; ++b) {
+            if ((float)s.window[b ^ 128] != 0.0f) p->zv = false;
+            if (p->h_inv[(size_t)m * 256 + b] >= 0) p->zv = false;
+        }
+    }
     // secondary contributions: ext slots numbered subband-major (a subband's
     // secondary bins are consecutive from its ext_base); the fix-up list is
     // ordered by contributor rank so shared bins are summed in a fixed order.

@@ -104,9 +104,6 @@ FCW_DI float2 zero2() { return make_float2(0.f, 0.f); }
 
 constexpr int kLtwLen = 64 + 4096 / 64;  // two-level long-transform twiddles (SMEM)
 constexpr int kTw16Len = 512;            // fft256_half per-lane twiddles (uniform L = 256 kernels)
-#ifndef FCW_RX_HYBRID
-#define FCW_RX_HYBRID 0  // fused RX L = 256: whole-warp tail round
-#endif
 #ifndef FCW_TX_TAIL2
 #define FCW_TX_TAIL2 1  // TX half-warp tail round: one subband per warp, one block per half
 #endif
@@ -349,7 +346,11 @@ FCW_DI void tx_short_warp(const KParams& P, const Team& tm, const SymDev& sy, co
 // (fc_sync.cpp:34-84: L/4 is a multiple of 16, so the circular shifts are
 // register renames) and the two block DFTs with their known-zero halves
 // pruned (block 1 lives on [L/4, 3L/4), block 0 on [L/4 - l_cp, 3L/4)).
-template <int N, int L>
+// ZV: every subband's bins t + 16m with m in [5, 10] are inactive (and
+// outside the window): those IDFT inputs are known zero (C5's centred 144 of
+// 256), so their gathers and first butterflies are skipped.
+constexpr unsigned long long kZ6 = 0x07E0ull;  // m = 5..10
+template <int N, int L, int ZV = 0>
 FCW_DI void tx_short_half(const KParams& P, const Team& tm, const SymDev& sy, const float2* __restrict__ row,
                           float2* spec0, float2* spec1, float2* scr, const float2* stw, int gstart, int gcount) {
     constexpr int TW = 16, PPT = L / TW;
@@ -374,24 +375,31 @@ FCW_DI void tx_short_half(const KParams& P, const Team& tm, const SymDev& sy, co
         float2 v[PPT];
         {
             const float2 ph = cscale(tw_conj(P.tw, theta_exp<N>(sd.cmodN, sy.smodN)), sd.tx_scale);
+            constexpr unsigned long long ZI = ZV ? kZ6 : 0ull;
+            auto live = [&](int k) { return !((ZI >> k) & 1ull); };
             int inv[PPT];
 #pragma unroll
-            for (int k = 0; k < PPT; ++k) inv[k] = act ? (int)(short)(__ldg(&ce[TW * k]).x & 0xffff) : -1;
+            for (int k = 0; k < PPT; ++k)
+                inv[k] = (act && live(k)) ? (int)(short)(__ldg(&ce[TW * k]).x & 0xffff) : -1;
             if (P.grid_full) {
                 const float2* g = row + sd.full_off + t;
 #pragma unroll
-                for (int k = 0; k < PPT; ++k) v[k] = act ? ld_stream(g + TW * k) : zero2();
+                for (int k = 0; k < PPT; ++k)
+                    if (live(k)) v[k] = act ? ld_stream(g + TW * k) : zero2();
             } else {
                 const float2* g = row + sd.act_off;
 #pragma unroll
-                for (int k = 0; k < PPT; ++k) v[k] = ld_stream(g + max(inv[k], 0));
+                for (int k = 0; k < PPT; ++k)
+                    if (live(k)) v[k] = ld_stream(g + max(inv[k], 0));
 #pragma unroll
-                for (int k = 0; k < PPT; ++k) v[k] = inv[k] >= 0 ? v[k] : zero2();
+                for (int k = 0; k < PPT; ++k)
+                    if (live(k)) v[k] = inv[k] >= 0 ? v[k] : zero2();
             }
 #pragma unroll
-            for (int k = 0; k < PPT; ++k) v[k] = cmul(v[k], ph);
+            for (int k = 0; k < PPT; ++k)
+                if (live(k)) v[k] = cmul(v[k], ph);
         }
-        fft256_half<+1>(v, buf, stw, t, 0, tw16_of(P, stw));  // x[t + 16 m] (scales folded into ph)
+        fft256_half<+1, ZV ? kZ6 : 0ull>(v, buf, stw, t, 0, tw16_of(P, stw));  // x[t + 16 m] (scales in ph)
         const int lcp = sy.cp >> sd.logI;
         const int qbase = sd.c - L / 2 + t, ext0 = N + sd.ext_base;
         const int r0 = pair ? 0 : h, r1 = pair ? 2 : h + 1;
@@ -426,7 +434,7 @@ FCW_DI void tx_short_half(const KParams& P, const Team& tm, const SymDev& sy, co
 
 // HALF: the kernel carries the half-warp twiddle table (the uniform L = 256
 // specialisation); generic kernels use the whole-warp lockstep path.
-template <int N, int L, bool HALF = false>
+template <int N, int L, bool HALF = false, int ZV = 0>
 FCW_DI void tx_short_one(const KParams& P, const Team& tm, const SymDev& sy, const float2* __restrict__ row,
                          const float2* __restrict__ row_next, bool staged, float2* spec0, float2* spec1,
                          float2* scr, const float2* stw, int gs, int gc) {
@@ -434,7 +442,7 @@ FCW_DI void tx_short_one(const KParams& P, const Team& tm, const SymDev& sy, con
         if constexpr (L <= 32)
             tx_short_thread<N, L>(P, tm, sy, row, spec0, spec1, gs, gc);
         else if constexpr (L == 256 && HALF)
-            tx_short_half<N, L>(P, tm, sy, row, spec0, spec1, scr, stw, gs, gc);
+            tx_short_half<N, L, ZV>(P, tm, sy, row, spec0, spec1, scr, stw, gs, gc);
         else if constexpr (L <= 256)
             tx_short_warp_lockstep<N, L>(P, tm, sy, row, spec0, spec1, scr, stw, gs, gc);
         else
@@ -583,7 +591,7 @@ FCW_DI void rx_short_team(const KParams& P, const Team& tm, const SymDev& sy, co
     }
 }
 
-template <int N, int LU>
+template <int N, int LU, int ZV = 0>
 FCW_DI void tx_short_all(const KParams& P, const Team& tm, const SymDev& sy, const float2* __restrict__ row,
                          const float2* __restrict__ row_next, bool staged, float2* spec0, float2* spec1,
                          float2* scr, const float2* stw) {
@@ -595,7 +603,7 @@ FCW_DI void tx_short_all(const KParams& P, const Team& tm, const SymDev& sy, con
             tx_short_one<N, LU>(P, tm, sy, row, row_next, staged, spec0, spec1, scr, stw, 0, P.M);
     } else if constexpr (LU > 0) {
         // uniform L: the next symbol's first subband is staged across calls
-        tx_short_one<N, LU, LU == 256>(P, tm, sy, row, row_next, staged, spec0, spec1, scr, stw, 0, P.M);
+        tx_short_one<N, LU, LU == 256, ZV>(P, tm, sy, row, row_next, staged, spec0, spec1, scr, stw, 0, P.M);
     } else {
         for (int g = 0; g < P.n_groups; ++g) {
             const int gs = P.grp_start[g], gc = P.grp_count[g];
@@ -790,7 +798,7 @@ FCW_DI void rx_short_warp(const KParams& P, const Team& tm, const SymDev& sy, co
 //     P1 = a conj(theta), P2 = s bp1 (-j)^t conj(theta) per lane and subband.
 // The spectra carry a wrap-around copy of bins [0, L) at [N, N + L), so the
 // bin addresses of a subband are one base plus immediate offsets.
-template <int N, int L>
+template <int N, int L, int ZV = 0>
 FCW_DI void rx_short_half(const KParams& P, const Team& tm, const SymDev& sy, const float2* spec0,
                           const float2* spec1, float2* __restrict__ orow, float2* scr, const float2* stw,
                           int gstart, int gcount) {
@@ -799,8 +807,10 @@ FCW_DI void rx_short_half(const KParams& P, const Team& tm, const SymDev& sy, co
     const int lane = threadIdx.x & 31, t = lane & (TW - 1), h = lane >> 4;
     float2* buf = scr + h * (P.scratch_stride / 2);
     const float sgn_t = (t & 1) ? -1.f : 1.f;  // (-1)^b
-    int done = 0;  // half-warp rounds (while more than one subband per warp remains if FCW_RX_HYBRID)
-    while (gcount - done > (FCW_RX_HYBRID ? tm.nwarp : 0)) {
+    // Rounds of two subbands per warp (a whole-warp tail round was measured
+    // slower here: the chain IDFT -> DFT cannot be split across halves).
+    int done = 0;
+    while (gcount - done > 0) {
         const int i = done + 2 * tm.warp + h;
         done += 2 * tm.nwarp;
         const bool act = i < gcount;
@@ -815,12 +825,16 @@ FCW_DI void rx_short_half(const KParams& P, const Team& tm, const SymDev& sy, co
         static_for<PPT>([&](auto kc) {
             constexpr int K = decltype(kc)::value;
             constexpr int KP = K ^ (PPT / 2);  // (t + 16K) ^ (L/2) == t + 16*KP
-            const float w = __int_as_float(__ldg(&ce[TW * K]).y);
-            const float2 a = s0[TW * KP], b = s1[TW * KP];
-            gw[K] = cscale(b, w);
-            f[K] = cscale(make_float2(fmaf(-sig, b.x, a.x), fmaf(-sig, b.y, a.y)), w);
+            if constexpr (ZV && ((kZ6 >> K) & 1ull)) {
+                gw[K] = zero2();  // outside every window: zero input, inactive output
+            } else {
+                const float w = __int_as_float(__ldg(&ce[TW * K]).y);
+                const float2 a = s0[TW * KP], b = s1[TW * KP];
+                gw[K] = cscale(b, w);
+                f[K] = cscale(make_float2(fmaf(-sig, b.x, a.x), fmaf(-sig, b.y, a.y)), w);
+            }
         });
-        fft256_half<+1>(f, buf, stw, t, L / 4, tw16_of(P, stw));  // IDFT of j^t f
+        fft256_half<+1, ZV ? kZ6 : 0ull>(f, buf, stw, t, L / 4, tw16_of(P, stw));  // IDFT of j^t f
         fft256_half<-1, 0xFF00ull>(f, buf, stw, t, 0, tw16_of(P, stw));  // S-hat keeps x[e], e < L/2; DFT
         const float2 ph = __ldg(&P.tw[theta_exp<N>(sd.cmodN, sy.smodN)]);  // conj(theta_n)
         const float2 P1 = cscale(ph, sd.rx_s0 / (float)L);
@@ -845,13 +859,11 @@ FCW_DI void rx_short_half(const KParams& P, const Team& tm, const SymDev& sy, co
             }
         }
     }
-    if (FCW_RX_HYBRID && done < gcount)
-        rx_short_warp<N, L>(P, tm, sy, spec0, spec1, orow, scr, stw, gstart + done, gcount - done);
 }
 
 // MIRROR: the kernel keeps the wrap-around spectrum copy rx_short_half needs
 // (the uniform L = 256 specialisation); generic kernels use the warp path.
-template <int N, int L, bool MIRROR = false>
+template <int N, int L, bool MIRROR = false, int ZV = 0>
 FCW_DI void rx_short_one(const KParams& P, const Team& tm, const SymDev& sy, const float2* spec0,
                          const float2* spec1, float2* orow, float2* scr, const float2* stw, int gs, int gc) {
     if constexpr (L <= N) {
@@ -859,7 +871,7 @@ FCW_DI void rx_short_one(const KParams& P, const Team& tm, const SymDev& sy, con
             rx_short_thread<N, L>(P, tm, sy, spec0, spec1, orow, gs, gc);
         else if constexpr (L == 256 && MIRROR) {
             if (P.fused)
-                rx_short_half<N, L>(P, tm, sy, spec0, spec1, orow, scr, stw, gs, gc);
+                rx_short_half<N, L, ZV>(P, tm, sy, spec0, spec1, orow, scr, stw, gs, gc);
             else
                 rx_short_warp<N, L>(P, tm, sy, spec0, spec1, orow, scr, stw, gs, gc);
         } else
@@ -867,7 +879,7 @@ FCW_DI void rx_short_one(const KParams& P, const Team& tm, const SymDev& sy, con
     }
 }
 
-template <int N, int LU>
+template <int N, int LU, int ZV = 0>
 FCW_DI void rx_short_all(const KParams& P, const Team& tm, const SymDev& sy, const float2* spec0,
                          const float2* spec1, float2* orow, float2* scr, const float2* stw) {
     if constexpr (use_team_short<N, LU>()) {
@@ -878,7 +890,7 @@ FCW_DI void rx_short_all(const KParams& P, const Team& tm, const SymDev& sy, con
         else
             rx_short_team<N, LU, teams_per_cta<N>(), false>(P, tm, sy, spec0, spec1, orow, scr);
     } else if constexpr (LU > 0) {
-        rx_short_one<N, LU, LU == 256>(P, tm, sy, spec0, spec1, orow, scr, stw, 0, P.M);
+        rx_short_one<N, LU, LU == 256, ZV>(P, tm, sy, spec0, spec1, orow, scr, stw, 0, P.M);
     } else {
         for (int g = 0; g < P.n_groups; ++g) {
             const int gs = P.grp_start[g], gc = P.grp_count[g];
@@ -993,7 +1005,7 @@ FCW_DI Smem smem_layout(const KParams& P, int g) {
     return s;
 }
 
-template <int N, int LU, bool DYN>
+template <int N, int LU, bool DYN, int ZV = 0>
 __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) tx_kernel(const KParams P) {
     constexpr int G = teams_per_cta<N>();
     constexpr int T = N / kPPT;                  // long-transform threads per team
@@ -1030,7 +1042,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) tx_kernel(const KP
             team_sync<G>(g, TT);  // previous symbol's transform no longer reads spec
             if (gtid == 0 && n + 1 < n1) prefetch_l2(in_u + (long long)(n + 1) * P.row_len, 8LL * P.row_len);
             if (!(P.dbg_skip & 1))
-                tx_short_all<N, LU>(P, tm, sy, in_u + (long long)n * P.row_len,
+                tx_short_all<N, LU, ZV>(P, tm, sy, in_u + (long long)n * P.row_len,
                                     n + 1 < n1 ? in_u + (long long)(n + 1) * P.row_len : nullptr, n > nfirst,
                                     spec0, spec1, S.scr, S.stw);
             team_sync<G>(g, TT);
@@ -1097,7 +1109,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) tx_kernel(const KP
     }
 }
 
-template <int N, int LU, bool DYN>
+template <int N, int LU, bool DYN, int ZV = 0>
 __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) rx_kernel(const KParams P) {
     constexpr int G = teams_per_cta<N>();
     constexpr int T = N / kPPT;
@@ -1163,7 +1175,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) rx_kernel(const KP
             }
             team_sync<G>(g, TT);
             if (!(P.dbg_skip & 1))
-                rx_short_all<N, LU>(P, tm, sy, spec0, spec1, out_u + (long long)n * P.row_len, S.scr, S.stw);
+                rx_short_all<N, LU, ZV>(P, tm, sy, spec0, spec1, out_u + (long long)n * P.row_len, S.scr, S.stw);
         }
     }
 }

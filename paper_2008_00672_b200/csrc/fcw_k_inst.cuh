@@ -11,3 +11,11 @@
         return KernelPair{tx_kernel<NN, LL, false>, rx_kernel<NN, LL, false>, tx_kernel<NN, LL, true>, \
                           rx_kernel<NN, LL, true>};                                             \
     }
+
+// ... and the variant whose subbands leave DFT bins t + 16m, m in [5, 10],
+// inactive and outside the window (ZV = 1, L = 256: see tx_short_half).
+#define FCW_KERNELS_NLZ(NN, LL)                                                                   \
+    KernelPair kernels_n##NN##_l##LL##z() {                                                       \
+        return KernelPair{tx_kernel<NN, LL, false, 1>, rx_kernel<NN, LL, false, 1>,              \
+                          tx_kernel<NN, LL, true, 1>, rx_kernel<NN, LL, true, 1>};               \
+    }

@@ -40,6 +40,7 @@ KernelPair kernels_n4096_l128();
 KernelPair kernels_n4096_l256();
 KernelPair kernels_n4096_l512();
 KernelPair kernels_n4096_l1024();
+KernelPair kernels_n4096_l256z();
 
 namespace {
 
@@ -64,7 +65,8 @@ KernelPair pick_l(int N, int LU) {
 #undef FCW_PICK_L
 }
 
-KernelPair pick(int N, int LU) {
+KernelPair pick(int N, int LU, bool zv = false) {
+    if (zv && N == 4096 && LU == 256) return kernels_n4096_l256z();
     switch (N) {
         case 16: return kernels_n16_l0();
         case 32: return kernels_n32_l0();
@@ -250,7 +252,7 @@ cudaError_t launch_tx(const Plan& p, KParams& kp, int S, cudaStream_t st) {
     kp.n_units = S;
     kp.teams = teams(p);
     kp.n_items = S * kp.nchunks;
-    const KernelPair kp2 = pick(p.N, LU);
+    const KernelPair kp2 = pick(p.N, LU, p.zv);
     return launch_one(kp.dynamic ? kp2.tx_d : kp2.tx, smem_bytes(p, true, false), kp, true, p.N, teams(p), st);
 }
 
@@ -262,7 +264,7 @@ cudaError_t launch_rx(const Plan& p, KParams& kp, int S, cudaStream_t st) {
     kp.n_units = S;
     kp.teams = teams(p);
     kp.n_items = S * kp.nchunks;
-    const KernelPair kp2 = pick(p.N, LU);
+    const KernelPair kp2 = pick(p.N, LU, p.zv);
     return launch_one(kp.dynamic ? kp2.rx_d : kp2.rx, smem_bytes(p, false, direct), kp, false, p.N, teams(p), st);
 }
 

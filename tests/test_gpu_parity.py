@@ -147,6 +147,7 @@ def _random_case(rng, N, Ls, cps):
     (2048, [1024, 512], [144] * 6),
     (4096, [32] * 7, [352, 288, 288, 288]),
     (4096, [1024, 64], [352, 288, 288]),
+    (4096, [256] * 3, [352, 288, 288, 288]),   # uniform L = 256 with full-support windows (no zero-bin variant)
 ])
 def test_random_geometries(N, Ls, cps):
     rng = np.random.default_rng(N + len(Ls))
