@@ -423,10 +423,12 @@ FCW_DI void tx_short_half(const KParams& P, const Team& tm, const SymDev& sy, co
             static_for<PPT>([&](auto kc) {
                 constexpr int K = decltype(kc)::value;
                 constexpr int KP = K ^ (PPT / 2);  // (t + 16K) ^ (L/2) == t + 16*KP
-                const int2 e = __ldg(&ce[TW * K]);
-                const int sec = e.x >> 16;
-                const int dest = sec >= 0 ? ext0 + sec : (sec == -1 ? ((qbase + TW * KP) & (N - 1)) : -1);
-                if (act && dest >= 0) spec[dest] = cscale(u[K], __int_as_float(e.y) * sgn);
+                if constexpr (!(ZV && ((kZ6 >> K) & 1ull))) {  // ZV: outside every window, no slot
+                    const int2 e = __ldg(&ce[TW * K]);
+                    const int sec = e.x >> 16;
+                    const int dest = sec >= 0 ? ext0 + sec : (sec == -1 ? ((qbase + TW * KP) & (N - 1)) : -1);
+                    if (act && dest >= 0) spec[dest] = cscale(u[K], __int_as_float(e.y) * sgn);
+                }
             });
         }
     }
@@ -850,12 +852,14 @@ FCW_DI void rx_short_half(const KParams& P, const Team& tm, const SymDev& sy, co
                 for (int k = 0; k < PPT; ++k) o[TW * k] = outv(k);
             } else {
                 float2* o = orow + sd.act_off;
+                constexpr unsigned long long ZO = ZV ? kZ6 : 0ull;  // ZV: inactive bins, nothing to store
                 int inv[PPT];  // all entry loads in flight before the first store
 #pragma unroll
-                for (int k = 0; k < PPT; ++k) inv[k] = (int)(short)(__ldg(&ce[TW * k]).x & 0xffff);
+                for (int k = 0; k < PPT; ++k)
+                    inv[k] = ((ZO >> k) & 1ull) ? -1 : (int)(short)(__ldg(&ce[TW * k]).x & 0xffff);
 #pragma unroll
                 for (int k = 0; k < PPT; ++k)
-                    if (inv[k] >= 0) o[inv[k]] = outv(k);
+                    if (!((ZO >> k) & 1ull) && inv[k] >= 0) o[inv[k]] = outv(k);
             }
         }
     }
