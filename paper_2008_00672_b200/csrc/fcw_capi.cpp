@@ -383,8 +383,23 @@ int fcw_plan_create(fcw_plan** out, int N, double overlap, const int* cp_high, i
         while (k < p->n_ext && secondary[order[k]].rank < l + 1) ++k;
         p->lvl_start[l] = k;
     }
+    // bins no subband touches; with the zero-bin variant the guard band
+    // [7N/16, 9N/16) is never read by the long transform (kernel skips it),
+    // so those bins go last and are not zero-filled (n_zero_core)
+    // (every bin a subband's L-span reads or writes lies outside the guard band)
+    p->zv = p->zv && [&] {
+        for (int m = 0; m < M; ++m)
+            for (int p0 = 0; p0 < sbs[m].L; ++p0) {
+                const int q = (int)mod_ll((long long)sbs[m].c - sbs[m].L / 2 + p0, N);
+                if (q >= 7 * N / 16 && q < 9 * N / 16) return false;
+            }
+        return true;
+    }();
     for (int q = 0; q < N; ++q)
-        if (cnt[q] == 0) p->h_zero.push_back(q);
+        if (cnt[q] == 0 && !(p->zv && q >= 7 * N / 16 && q < 9 * N / 16)) p->h_zero.push_back(q);
+    p->n_zero_core = (int)p->h_zero.size();
+    for (int q = 0; q < N; ++q)
+        if (cnt[q] == 0 && p->zv && q >= 7 * N / 16 && q < 9 * N / 16) p->h_zero.push_back(q);
     // L groups
     std::map<int, std::vector<int>> groups;
     for (int m = 0; m < M; ++m) groups[sbs[m].L].push_back(m);

@@ -1074,19 +1074,24 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) tx_kernel(const KP
                 const int u = gtid + T * m;
                 cr[m] = (act && n > nfirst && u < sy.carry_len) ? carry[u] : zero2();
             }
+            // zv plans: no subband touches the guard band [7N/16, 9N/16), i.e.
+            // elements m = 7, 8 of every thread (T = N/16): known-zero inputs
+            constexpr unsigned long long ZG = (ZV && N == 4096) ? 0x0180ull : 0ull;
             float2 v[2][kPPT];
             if (act) {
 #pragma unroll
                 for (int m = 0; m < kPPT; ++m) {
-                    v[0][m] = spec0[gtid + T * m];
-                    v[1][m] = spec1[gtid + T * m];
+                    if (!((ZG >> m) & 1ull)) {
+                        v[0][m] = spec0[gtid + T * m];
+                        v[1][m] = spec1[gtid + T * m];
+                    }
                 }
             }
             {
                 float2* const bufs[2] = {spec0, spec1};
                 if (!(P.dbg_skip & 2))
-                    team_fft<N, T, kPPT, +1, 2, true, long_twl<N>()>(v, bufs, long_twl<N>() ? S.ltw : P.tw, 1, gtid, act,
-                                                                    G == 1 ? 0 : 1 + g, TT);
+                    team_fft<N, T, kPPT, +1, 2, true, long_twl<N>(), ZG>(v, bufs, long_twl<N>() ? S.ltw : P.tw, 1,
+                                                                        gtid, act, G == 1 ? 0 : 1 + g, TT);
             }
             // every thread has read its carry before it is overwritten: the long
             // transform's exchange barriers already order that for N >= 512

@@ -261,7 +261,7 @@ FCW_DI void twiddle_powers(float2 (&w)[R], const float2* tw, int e0) {
 }
 
 // One Stockham pass (and the remaining ones, recursively).
-template <int n, int T, int PPT, int SIGN, int NF, bool CTA, int NS, int TWL>
+template <int n, int T, int PPT, int SIGN, int NF, bool CTA, int NS, int TWL, unsigned long long ZIN0 = 0>
 FCW_DI void team_pass(float2 (&v)[NF][PPT], float2* const* buf, const float2* __restrict__ tw,
                       int ts, int t, bool act, int bar_id, int bar_n) {
     constexpr int R0 = PPT < 16 ? PPT : 16;
@@ -289,7 +289,7 @@ FCW_DI void team_pass(float2 (&v)[NF][PPT], float2* const* buf, const float2* __
                     for (int f = 0; f < NF; ++f) y[f][k] = cmul(y[f][k], wk[k]);
             }
 #pragma unroll
-            for (int f = 0; f < NF; ++f) fft_reg<R, SIGN>(y[f]);
+            for (int f = 0; f < NF; ++f) fft_reg<R, SIGN, NS == 1 && NB == 1 ? ZIN0 : 0ull>(y[f]);
 #pragma unroll
             for (int f = 0; f < NF; ++f)
 #pragma unroll
@@ -324,7 +324,8 @@ FCW_DI void team_pass(float2 (&v)[NF][PPT], float2* const* buf, const float2* __
 // thread of the block) must call it; threads with act == false only join the
 // barriers.  The buffers must hold spad(n) + 1 float2 each and may alias the
 // input's source memory once it has been read into v.
-template <int n, int T, int PPT, int SIGN, int NF, bool CTA, int TWL = 0>
+// ZIN0: inputs v[f][m] known to be zero (first pass, one butterfly per thread).
+template <int n, int T, int PPT, int SIGN, int NF, bool CTA, int TWL = 0, unsigned long long ZIN0 = 0>
 FCW_DI void team_fft(float2 (&v)[NF][PPT], float2* const* buf, const float2* __restrict__ tw, int ts,
                      int t, bool act, int bar_id = 0, int bar_n = 0) {
     static_assert(n == T * PPT, "team_fft: n != T*PPT");
@@ -335,7 +336,7 @@ FCW_DI void team_fft(float2 (&v)[NF][PPT], float2* const* buf, const float2* __r
             for (int f = 0; f < NF; ++f) fft_reg<PPT, SIGN>(v[f]);
         }
     } else {
-        team_pass<n, T, PPT, SIGN, NF, CTA, 1, TWL>(v, buf, tw, ts, t, act, bar_id, bar_n);
+        team_pass<n, T, PPT, SIGN, NF, CTA, 1, TWL, ZIN0>(v, buf, tw, ts, t, act, bar_id, bar_n);
     }
 }
 

@@ -115,7 +115,8 @@ struct Plan {
     int n_groups = 0;
     int grp_L[kMaxGroups]{}, grp_start[kMaxGroups]{}, grp_count[kMaxGroups]{};
     int Lmax = 0;
-    bool zv = false;  // uniform L = 256, N = 4096, bins t + 16m (m in [5, 10]) inactive and windowed out
+    bool zv = false;
+    int n_zero_core = 0;  // zero-filled bins (the guard band of a zv plan excluded)  // uniform L = 256, N = 4096, bins t + 16m (m in [5, 10]) inactive and windowed out
     // device tables (one allocation)
     void* d_blob = nullptr;
     SubDev* d_sub = nullptr;

@@ -215,7 +215,7 @@ void fill_common(const Plan& p, KParams& kp) {
     kp.M = p.M;
     kp.spec_stride = spec_stride(p);
     kp.n_ext = p.n_ext;
-    kp.n_zero = (int)p.h_zero.size();
+    kp.n_zero = p.zv ? p.n_zero_core : (int)p.h_zero.size();  // zv kernels never read the guard band
     kp.n_lvl = p.n_lvl;
     for (int i = 0; i <= kMaxLevels; ++i) kp.lvl_start[i] = i < (int)p.lvl_start.size() ? p.lvl_start[i] : p.n_ext;
     kp.n_groups = p.n_groups;
