@@ -417,7 +417,8 @@ FCW_DI void tx_short_half(const KParams& P, const Team& tm, const SymDev& sy, co
                 else
                     u[k] = zero2();  // k >= 12: known zero (not read)
             }
-            fft256_half<-1, 0xF000ull>(u, buf, stw, t, 0, tw16_of(P, stw));
+            // ZV: block bins t + 16m, m in [5, 10], lie outside every window (never scattered)
+            fft256_half<-1, 0xF000ull, ZV ? (0xFFFFull & ~kZ6) : ~0ull>(u, buf, stw, t, 0, tw16_of(P, stw));
             float2* spec = r ? spec1 : spec0;
             const float sgn = r ? sd.bp1 : 1.f;
             static_for<PPT>([&](auto kc) {
@@ -836,7 +837,8 @@ FCW_DI void rx_short_half(const KParams& P, const Team& tm, const SymDev& sy, co
                 f[K] = cscale(make_float2(fmaf(-sig, b.x, a.x), fmaf(-sig, b.y, a.y)), w);
             }
         });
-        fft256_half<+1, ZV ? kZ6 : 0ull>(f, buf, stw, t, L / 4, tw16_of(P, stw));  // IDFT of j^t f
+        // IDFT of j^t f; S-hat then keeps x[e], e < L/2: outputs m >= 8 are dead
+        fft256_half<+1, ZV ? kZ6 : 0ull, 0x00FFull>(f, buf, stw, t, L / 4, tw16_of(P, stw));
         fft256_half<-1, 0xFF00ull>(f, buf, stw, t, 0, tw16_of(P, stw));  // S-hat keeps x[e], e < L/2; DFT
         const float2 ph = __ldg(&P.tw[theta_exp<N>(sd.cmodN, sy.smodN)]);  // conj(theta_n)
         const float2 P1 = cscale(ph, sd.rx_s0 / (float)L);

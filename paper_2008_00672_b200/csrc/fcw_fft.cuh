@@ -122,7 +122,9 @@ __host__ __device__ constexpr unsigned long long zm_brev(unsigned long long zm, 
     return out;
 }
 
-template <int L, int SIGN, int LEN, int K, unsigned long long ZM = 0>
+// OM: outputs (natural order) the caller needs; in the last stage a butterfly
+// with one dead output computes only the other.
+template <int L, int SIGN, int LEN, int K, unsigned long long ZM = 0, unsigned long long OM = ~0ull>
 FCW_DI void fft_stage(float2 (&x)[L]) {
     if constexpr (LEN <= L) {
         if constexpr (K < LEN / 2) {
@@ -132,7 +134,16 @@ FCW_DI void fft_stage(float2 (&x)[L]) {
                 const float2 a = x[s + K];
                 const float2 b = x[s + K + H];
                 const bool za = (ZM >> (s + K)) & 1ull, zb = (ZM >> (s + K + H)) & 1ull;
-                if (za && zb) {
+                const bool n0 = LEN < L || ((OM >> (s + K)) & 1ull), n1 = LEN < L || ((OM >> (s + K + H)) & 1ull);
+                if (!n0 && !n1) {
+                    // neither output used
+                } else if (!(za || zb) && !(n0 && n1)) {
+                    // one live output: y = a +- w b
+                    float2 wb = b;
+                    if constexpr (K != 0) wb = cmul(b, make_float2(Tw<LEN, K, SIGN>::re, Tw<LEN, K, SIGN>::im));
+                    if (n0) x[s + K] = cadd(a, wb);
+                    else x[s + K + H] = csub(a, wb);
+                } else if (za && zb) {
                     x[s + K] = make_float2(0.f, 0.f);  // never read the (unset) zero registers
                     x[s + K + H] = make_float2(0.f, 0.f);
                 } else if (zb) {
@@ -168,15 +179,15 @@ FCW_DI void fft_stage(float2 (&x)[L]) {
                     x[s + K + H] = make_float2(fmaf(2.f, a.x, -y0r), fmaf(2.f, a.y, -y0i));
                 }
             }
-            fft_stage<L, SIGN, LEN, K + 1, ZM>(x);
+            fft_stage<L, SIGN, LEN, K + 1, ZM, OM>(x);
         } else {
-            fft_stage<L, SIGN, LEN * 2, 0, zm_next(ZM, L, LEN)>(x);
+            fft_stage<L, SIGN, LEN * 2, 0, zm_next(ZM, L, LEN), OM>(x);
         }
     }
 }
 
 // ZIN: compile-time mask of inputs (natural order) known to be zero.
-template <int L, int SIGN, unsigned long long ZIN = 0>
+template <int L, int SIGN, unsigned long long ZIN = 0, unsigned long long OM = ~0ull>
 FCW_DI void fft_reg(float2 (&x)[L]) {
     if constexpr (L == 1) return;
     constexpr int LB = cx_log2(L);
@@ -189,7 +200,7 @@ FCW_DI void fft_reg(float2 (&x)[L]) {
             x[j] = t;
         }
     }
-    fft_stage<L, SIGN, 2, 0, zm_brev(ZIN, L, LB)>(x);
+    fft_stage<L, SIGN, 2, 0, zm_brev(ZIN, L, LB), OM>(x);
 }
 
 // ------------------------------------------------------------ team barriers
@@ -354,7 +365,8 @@ FCW_DI void team_fft(float2 (&v)[NF][PPT], float2* const* buf, const float2* __r
 // tw16 (optional): per-lane twiddle table, tw16[sel][m][t] = exp(-2 pi i m (t + 64 sel) / 256)
 // for sel = eoff / 64 in {0, 1}: 15 conflict-free loads instead of 4 loads
 // and 11 complex products.
-template <int SIGN, unsigned long long ZIN = 0>
+// OUT: outputs v[k] the caller uses (dead ones are not computed).
+template <int SIGN, unsigned long long ZIN = 0, unsigned long long OUT = ~0ull>
 FCW_DI void fft256_half(float2 (&v)[16], float2* buf, const float2* stw, int t, int eoff,
                         const float2* tw16 = nullptr) {
     fft_reg<16, SIGN, ZIN>(v);
@@ -374,7 +386,7 @@ FCW_DI void fft256_half(float2 (&v)[16], float2* buf, const float2* stw, int t, 
             if constexpr (SIGN > 0) w.y = -w.y;
             v[m] = cmul(v[m], w);
         }
-        fft_reg<16, SIGN>(v);
+        fft_reg<16, SIGN, 0ull, OUT>(v);
         return;
     }
     const int e0 = (t + eoff) & 255;
@@ -396,7 +408,7 @@ FCW_DI void fft256_half(float2 (&v)[16], float2* buf, const float2* stw, int t, 
     for (int k = 9; k < 16; ++k) w[k] = cmul(w[k - 8], w[8]);
 #pragma unroll
     for (int m = 1; m < 16; ++m) v[m] = cmul(v[m], w[m]);
-    fft_reg<16, SIGN>(v);
+    fft_reg<16, SIGN, 0ull, OUT>(v);
 }
 
 }  // namespace fcw
