@@ -395,11 +395,36 @@ int fcw_plan_create(fcw_plan** out, int N, double overlap, const int* cp_high, i
             }
         return true;
     }();
+    // narrowband plans (config 1): every subband span inside 16 bins [k0, k0 + 16)
+    // of N = 1024 with L = 16 -> per-thread 16-point long transforms (ZV = 2)
+    p->nb = false;
+    if (N == 1024) {
+        bool uni16 = true;
+        for (int m = 0; m < M; ++m) uni16 = uni16 && sbs[m].L == 16;
+        if (uni16) {
+            std::vector<int> span;
+            for (int m = 0; m < M; ++m)
+                for (int p0 = 0; p0 < 16; ++p0) span.push_back((int)mod_ll((long long)sbs[m].c - 8 + p0, N));
+            for (int k0 : span) {
+                bool ok = true;
+                for (int q : span) ok = ok && mod_ll((long long)q - k0, N) < 16;
+                if (ok) {
+                    p->nb = true;
+                    p->nb_k0 = k0;
+                    break;
+                }
+            }
+        }
+    }
+    auto core = [&](int q) {
+        if (p->nb) return mod_ll((long long)q - p->nb_k0, N) < 16;
+        return !(p->zv && q >= 7 * N / 16 && q < 9 * N / 16);
+    };
     for (int q = 0; q < N; ++q)
-        if (cnt[q] == 0 && !(p->zv && q >= 7 * N / 16 && q < 9 * N / 16)) p->h_zero.push_back(q);
+        if (cnt[q] == 0 && core(q)) p->h_zero.push_back(q);
     p->n_zero_core = (int)p->h_zero.size();
     for (int q = 0; q < N; ++q)
-        if (cnt[q] == 0 && p->zv && q >= 7 * N / 16 && q < 9 * N / 16) p->h_zero.push_back(q);
+        if (cnt[q] == 0 && !core(q)) p->h_zero.push_back(q);
     // L groups
     std::map<int, std::vector<int>> groups;
     for (int m = 0; m < M; ++m) groups[sbs[m].L].push_back(m);

@@ -375,7 +375,7 @@ FCW_DI void tx_short_half(const KParams& P, const Team& tm, const SymDev& sy, co
         float2 v[PPT];
         {
             const float2 ph = cscale(tw_conj(P.tw, theta_exp<N>(sd.cmodN, sy.smodN)), sd.tx_scale);
-            constexpr unsigned long long ZI = ZV ? kZ6 : 0ull;
+            constexpr unsigned long long ZI = ZV == 1 ? kZ6 : 0ull;
             auto live = [&](int k) { return !((ZI >> k) & 1ull); };
             int inv[PPT];
 #pragma unroll
@@ -399,7 +399,7 @@ FCW_DI void tx_short_half(const KParams& P, const Team& tm, const SymDev& sy, co
             for (int k = 0; k < PPT; ++k)
                 if (live(k)) v[k] = cmul(v[k], ph);
         }
-        fft256_half<+1, ZV ? kZ6 : 0ull>(v, buf, stw, t, 0, tw16_of(P, stw));  // x[t + 16 m] (scales in ph)
+        fft256_half<+1, ZV == 1 ? kZ6 : 0ull>(v, buf, stw, t, 0, tw16_of(P, stw));  // x[t + 16 m] (scales in ph)
         const int lcp = sy.cp >> sd.logI;
         const int qbase = sd.c - L / 2 + t, ext0 = N + sd.ext_base;
         const int r0 = pair ? 0 : h, r1 = pair ? 2 : h + 1;
@@ -418,13 +418,13 @@ FCW_DI void tx_short_half(const KParams& P, const Team& tm, const SymDev& sy, co
                     u[k] = zero2();  // k >= 12: known zero (not read)
             }
             // ZV: block bins t + 16m, m in [5, 10], lie outside every window (never scattered)
-            fft256_half<-1, 0xF000ull, ZV ? (0xFFFFull & ~kZ6) : ~0ull>(u, buf, stw, t, 0, tw16_of(P, stw));
+            fft256_half<-1, 0xF000ull, ZV == 1 ? (0xFFFFull & ~kZ6) : ~0ull>(u, buf, stw, t, 0, tw16_of(P, stw));
             float2* spec = r ? spec1 : spec0;
             const float sgn = r ? sd.bp1 : 1.f;
             static_for<PPT>([&](auto kc) {
                 constexpr int K = decltype(kc)::value;
                 constexpr int KP = K ^ (PPT / 2);  // (t + 16K) ^ (L/2) == t + 16*KP
-                if constexpr (!(ZV && ((kZ6 >> K) & 1ull))) {  // ZV: outside every window, no slot
+                if constexpr (!(ZV == 1 && ((kZ6 >> K) & 1ull))) {  // ZV: outside every window, no slot
                     const int2 e = __ldg(&ce[TW * K]);
                     const int sec = e.x >> 16;
                     const int dest = sec >= 0 ? ext0 + sec : (sec == -1 ? ((qbase + TW * KP) & (N - 1)) : -1);
@@ -828,7 +828,7 @@ FCW_DI void rx_short_half(const KParams& P, const Team& tm, const SymDev& sy, co
         static_for<PPT>([&](auto kc) {
             constexpr int K = decltype(kc)::value;
             constexpr int KP = K ^ (PPT / 2);  // (t + 16K) ^ (L/2) == t + 16*KP
-            if constexpr (ZV && ((kZ6 >> K) & 1ull)) {
+            if constexpr (ZV == 1 && ((kZ6 >> K) & 1ull)) {
                 gw[K] = zero2();  // outside every window: zero input, inactive output
             } else {
                 const float w = __int_as_float(__ldg(&ce[TW * K]).y);
@@ -838,7 +838,7 @@ FCW_DI void rx_short_half(const KParams& P, const Team& tm, const SymDev& sy, co
             }
         });
         // IDFT of j^t f; S-hat then keeps x[e], e < L/2: outputs m >= 8 are dead
-        fft256_half<+1, ZV ? kZ6 : 0ull, 0x00FFull>(f, buf, stw, t, L / 4, tw16_of(P, stw));
+        fft256_half<+1, ZV == 1 ? kZ6 : 0ull, 0x00FFull>(f, buf, stw, t, L / 4, tw16_of(P, stw));
         fft256_half<-1, 0xFF00ull>(f, buf, stw, t, 0, tw16_of(P, stw));  // S-hat keeps x[e], e < L/2; DFT
         const float2 ph = __ldg(&P.tw[theta_exp<N>(sd.cmodN, sy.smodN)]);  // conj(theta_n)
         const float2 P1 = cscale(ph, sd.rx_s0 / (float)L);
@@ -854,7 +854,7 @@ FCW_DI void rx_short_half(const KParams& P, const Team& tm, const SymDev& sy, co
                 for (int k = 0; k < PPT; ++k) o[TW * k] = outv(k);
             } else {
                 float2* o = orow + sd.act_off;
-                constexpr unsigned long long ZO = ZV ? kZ6 : 0ull;  // ZV: inactive bins, nothing to store
+                constexpr unsigned long long ZO = ZV == 1 ? kZ6 : 0ull;  // ZV: inactive bins, nothing to store
                 int inv[PPT];  // all entry loads in flight before the first store
 #pragma unroll
                 for (int k = 0; k < PPT; ++k)
@@ -932,6 +932,103 @@ FCW_DI void team_sync(int g, int nthr) {
         __syncthreads();
     else
         asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(nthr) : "memory");
+}
+
+// ------------------------------------------------ narrowband long transforms
+// ZV == 2: every subband's L-bin span lies in the 16 bins [k0, k0 + 16) (mod
+// N) — config 1, one 12-subcarrier subband in N = 1024.  The N-point transform
+// of a block then collapses to one 16-point transform per thread with input
+// and output twiddles (the pruned IDFT_N of SURVEY §7 hard part 1e): no SMEM
+// exchange passes.  Thread t holds x[t + T s], s < 16, T = N / 16.
+
+// p[k] = u^k for k < 16, each at most three products deep.
+FCW_DI void cpow16(float2 (&p)[16], float2 u) {
+    p[0] = make_float2(1.f, 0.f);
+    p[1] = u;
+    p[2] = cmul(u, u);
+    p[3] = cmul(p[2], u);
+    p[4] = cmul(p[2], p[2]);
+#pragma unroll
+    for (int k = 5; k < 8; ++k) p[k] = cmul(p[4], p[k - 4]);
+    p[8] = cmul(p[4], p[4]);
+#pragma unroll
+    for (int k = 9; k < 16; ++k) p[k] = cmul(p[8], p[k - 8]);
+}
+
+// TX: x_f[t + T s] = sum_k S_f[k0 + k] e^{+2 pi i (t + T s)(k0 + k) / N}
+//   = E(t k0) w16^{s k0} IDFT16_s(S_f[k0 + k] E(t k)),  E(a) = e^{2 pi i a / N}.
+template <int N>
+FCW_DI void nb_long_inverse(float2 (&v)[2][16], const float2* spec0, const float2* spec1, const float2* tw,
+                            int t, int k0) {
+    constexpr int T = N / 16;
+    float2 w[16], q[16];
+    cpow16(w, tw_conj(tw, t));  // E(t)^k
+#pragma unroll
+    for (int f = 0; f < 2; ++f) {
+        const float2* S = f ? spec1 : spec0;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) v[f][k] = cmul(S[(k0 + k) & (N - 1)], w[k]);
+        fft_reg<16, +1>(v[f]);
+    }
+    cpow16(q, tw_conj(tw, (T * k0) & (N - 1)));  // w16^{s k0}
+    const float2 c = tw_conj(tw, (int)(((unsigned)t * (unsigned)k0) & (unsigned)(N - 1)));
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {
+        const float2 ps = cmul(q[s], c);
+        v[0][s] = cmul(v[0][s], ps);
+        v[1][s] = cmul(v[1][s], ps);
+    }
+}
+
+// RX: Y_f[k0 + k] = sum_t W^{t(k0 + k)} DFT16_k(y_f[t + T s] W16^{s k0}),
+// W = e^{-2 pi i / N}; the sum over the T threads goes through SMEM
+// (red: 32 T float2, the team's spectrum region) in a fixed order.
+template <int N, int G>
+FCW_DI void nb_long_forward(float2 (&v)[2][16], float2* spec0, float2* spec1, float2* red, const float2* tw, int t,
+                            int k0, int g, int TT) {
+    constexpr int T = N / 16;
+    static_assert(T >= 64 && T % 32 == 0, "narrowband reduction: T = N / 16 >= 64");
+    float2 q[16], w[16];
+    cpow16(q, __ldg(&tw[(T * k0) & (N - 1)]));  // W16^{s k0}
+#pragma unroll
+    for (int s = 1; s < 16; ++s) {
+        v[0][s] = cmul(v[0][s], q[s]);
+        v[1][s] = cmul(v[1][s], q[s]);
+    }
+    fft_reg<16, -1>(v[0]);
+    fft_reg<16, -1>(v[1]);
+    cpow16(w, __ldg(&tw[t]));  // W^{t k}
+    const float2 c = __ldg(&tw[(int)(((unsigned)t * (unsigned)k0) & (unsigned)(N - 1))]);
+    // partials thread-major, padded (conflict-free): red[t * 33 + p], p = 16 f + k
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        const float2 pk = cmul(w[k], c);
+        red[t * 33 + k] = cmul(v[0][k], pk);
+        red[t * 33 + 16 + k] = cmul(v[1][k], pk);
+    }
+    team_sync<G>(g, TT);
+    // warp w sums the partials of threads [32 w, 32 w + 32), lane = p
+    constexpr int W = T / 32;
+    const int lane = t & 31, wp = t >> 5;
+    float2 a0 = zero2(), a1 = zero2(), a2 = zero2(), a3 = zero2();
+    const float2* src = red + (32 * wp) * 33 + lane;
+#pragma unroll
+    for (int j = 0; j < 32; j += 4) {
+        a0 = cadd(a0, src[(j + 0) * 33]);
+        a1 = cadd(a1, src[(j + 1) * 33]);
+        a2 = cadd(a2, src[(j + 2) * 33]);
+        a3 = cadd(a3, src[(j + 3) * 33]);
+    }
+    float2* accs = red + T * 33;  // W x 32 warp sums
+    accs[wp * 32 + lane] = cadd(cadd(a0, a1), cadd(a2, a3));
+    team_sync<G>(g, TT);
+    if (wp == 0) {
+        float2 y = accs[lane];
+#pragma unroll
+        for (int q = 1; q < W; ++q) y = cadd(y, accs[q * 32 + lane]);
+        float2* S = lane < 16 ? spec0 : spec1;
+        S[(k0 + (lane & 15)) & (N - 1)] = y;
+    }
 }
 
 // Work distribution over the resident teams, two modes (chosen per launch):
@@ -1078,18 +1175,22 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) tx_kernel(const KP
             }
             // zv plans: no subband touches the guard band [7N/16, 9N/16), i.e.
             // elements m = 7, 8 of every thread (T = N/16): known-zero inputs
-            constexpr unsigned long long ZG = (ZV && N == 4096) ? 0x0180ull : 0ull;
+            constexpr unsigned long long ZG = (ZV == 1 && N == 4096) ? 0x0180ull : 0ull;
             float2 v[2][kPPT];
-            if (act) {
+            if constexpr (ZV == 2) {
+                // narrowband plan: one 16-point transform per thread (no exchange)
+                if (act) nb_long_inverse<N>(v, spec0, spec1, P.tw, gtid, P.nb_k0);
+                team_sync<G>(g, TT);  // the spectra are read before the next symbol rewrites them
+            } else {
+                if (act) {
 #pragma unroll
-                for (int m = 0; m < kPPT; ++m) {
-                    if (!((ZG >> m) & 1ull)) {
-                        v[0][m] = spec0[gtid + T * m];
-                        v[1][m] = spec1[gtid + T * m];
+                    for (int m = 0; m < kPPT; ++m) {
+                        if (!((ZG >> m) & 1ull)) {
+                            v[0][m] = spec0[gtid + T * m];
+                            v[1][m] = spec1[gtid + T * m];
+                        }
                     }
                 }
-            }
-            {
                 float2* const bufs[2] = {spec0, spec1};
                 if (!(P.dbg_skip & 2))
                     team_fft<N, T, kPPT, +1, 2, true, long_twl<N>(), ZG>(v, bufs, long_twl<N>() ? S.ltw : P.tw, 1,
@@ -1163,6 +1264,11 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) rx_kernel(const KP
                 }
             }
             team_sync<G>(g, TT);  // previous symbol's subband stage no longer reads spec
+            if constexpr (ZV == 2) {
+                // narrowband plan: 16-point transforms per thread + a fixed-order sum
+                // over the team; only bins [k0, k0 + 16) are produced
+                nb_long_forward<N, G>(v, spec0, spec1, spec0, P.tw, gtid, P.nb_k0, g, TT);
+            } else {
             {
                 float2* const bufs[2] = {spec0, spec1};
                 if (!(P.dbg_skip & 2))
@@ -1183,6 +1289,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) rx_kernel(const KP
                         }
                     }
                 }
+            }
             }
             team_sync<G>(g, TT);
             if (!(P.dbg_skip & 1))

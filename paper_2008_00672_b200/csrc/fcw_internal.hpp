@@ -58,6 +58,7 @@ struct KParams {
     int stab_len;        // entries of the SMEM short-transform twiddle table (plan Lmax)
     int stage_off;       // TX: offset of the cp.async grid staging buffer in a warp's scratch
     int tw16_len;        // float2 entries of the half-warp FFT_256 twiddle table in SMEM (0 or 512)
+    int nb_k0;           // narrowband plans (ZV == 2 kernels): first of the 16 spectrum bins in use
     int row_len;
     int grid_full;
     int fused;
@@ -116,7 +117,9 @@ struct Plan {
     int grp_L[kMaxGroups]{}, grp_start[kMaxGroups]{}, grp_count[kMaxGroups]{};
     int Lmax = 0;
     bool zv = false;
-    int n_zero_core = 0;  // zero-filled bins (the guard band of a zv plan excluded)  // uniform L = 256, N = 4096, bins t + 16m (m in [5, 10]) inactive and windowed out
+    int n_zero_core = 0;  // zero-filled bins (the guard band of a zv plan excluded)
+    bool nb = false;      // narrowband: every subband span within 16 bins [nb_k0, nb_k0 + 16), N = 1024, L = 16
+    int nb_k0 = 0;  // uniform L = 256, N = 4096, bins t + 16m (m in [5, 10]) inactive and windowed out
     // device tables (one allocation)
     void* d_blob = nullptr;
     SubDev* d_sub = nullptr;

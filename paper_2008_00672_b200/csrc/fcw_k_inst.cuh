@@ -19,3 +19,10 @@
         return KernelPair{tx_kernel<NN, LL, false, 1>, rx_kernel<NN, LL, false, 1>,              \
                           tx_kernel<NN, LL, true, 1>, rx_kernel<NN, LL, true, 1>};               \
     }
+
+// ... and the narrowband variant (ZV = 2: every subband span inside 16 bins).
+#define FCW_KERNELS_NLN(NN, LL)                                                                   \
+    KernelPair kernels_n##NN##_l##LL##n() {                                                       \
+        return KernelPair{tx_kernel<NN, LL, false, 2>, rx_kernel<NN, LL, false, 2>,              \
+                          tx_kernel<NN, LL, true, 2>, rx_kernel<NN, LL, true, 2>};               \
+    }

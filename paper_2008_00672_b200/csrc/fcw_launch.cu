@@ -41,6 +41,7 @@ KernelPair kernels_n4096_l256();
 KernelPair kernels_n4096_l512();
 KernelPair kernels_n4096_l1024();
 KernelPair kernels_n4096_l256z();
+KernelPair kernels_n1024_l16n();
 
 namespace {
 
@@ -65,8 +66,9 @@ KernelPair pick_l(int N, int LU) {
 #undef FCW_PICK_L
 }
 
-KernelPair pick(int N, int LU, bool zv = false) {
+KernelPair pick(int N, int LU, bool zv = false, bool nb = false) {
     if (zv && N == 4096 && LU == 256) return kernels_n4096_l256z();
+    if (nb && N == 1024 && LU == 16) return kernels_n1024_l16n();
     switch (N) {
         case 16: return kernels_n16_l0();
         case 32: return kernels_n32_l0();
@@ -215,7 +217,9 @@ void fill_common(const Plan& p, KParams& kp) {
     kp.M = p.M;
     kp.spec_stride = spec_stride(p);
     kp.n_ext = p.n_ext;
-    kp.n_zero = p.zv ? p.n_zero_core : (int)p.h_zero.size();  // zv kernels never read the guard band
+    // zv kernels never read the guard band, narrowband kernels only bins [nb_k0, nb_k0 + 16)
+    kp.n_zero = (p.zv || p.nb) ? p.n_zero_core : (int)p.h_zero.size();
+    kp.nb_k0 = p.nb_k0;
     kp.n_lvl = p.n_lvl;
     for (int i = 0; i <= kMaxLevels; ++i) kp.lvl_start[i] = i < (int)p.lvl_start.size() ? p.lvl_start[i] : p.n_ext;
     kp.n_groups = p.n_groups;
@@ -252,7 +256,7 @@ cudaError_t launch_tx(const Plan& p, KParams& kp, int S, cudaStream_t st) {
     kp.n_units = S;
     kp.teams = teams(p);
     kp.n_items = S * kp.nchunks;
-    const KernelPair kp2 = pick(p.N, LU, p.zv);
+    const KernelPair kp2 = pick(p.N, LU, p.zv, p.nb);
     return launch_one(kp.dynamic ? kp2.tx_d : kp2.tx, smem_bytes(p, true, false), kp, true, p.N, teams(p), st);
 }
 
@@ -264,7 +268,7 @@ cudaError_t launch_rx(const Plan& p, KParams& kp, int S, cudaStream_t st) {
     kp.n_units = S;
     kp.teams = teams(p);
     kp.n_items = S * kp.nchunks;
-    const KernelPair kp2 = pick(p.N, LU, p.zv);
+    const KernelPair kp2 = pick(p.N, LU, p.zv, p.nb);
     return launch_one(kp.dynamic ? kp2.rx_d : kp2.rx, smem_bytes(p, false, direct), kp, false, p.N, teams(p), st);
 }
 

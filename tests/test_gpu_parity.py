@@ -148,6 +148,7 @@ def _random_case(rng, N, Ls, cps):
     (4096, [32] * 7, [352, 288, 288, 288]),
     (4096, [1024, 64], [352, 288, 288]),
     (4096, [256] * 3, [352, 288, 288, 288]),   # uniform L = 256 with full-support windows (no zero-bin variant)
+    (1024, [16], [80, 72, 72]),                # one L = 16 subband: narrowband long transforms
 ])
 def test_random_geometries(N, Ls, cps):
     rng = np.random.default_rng(N + len(Ls))
@@ -241,3 +242,28 @@ def test_tx_accumulate_adds():
     plan.tx(grid, b, S, accumulate=True)
     torch.cuda.synchronize()
     assert torch.allclose(b, 2 * a, rtol=1e-6, atol=1e-7)
+
+
+def test_narrowband_wrapping_span():
+    """N = 1024, one L = 16 subband whose 16-bin span wraps through bin 0: the
+    narrowband long transforms (k0 = c - 8 mod N) against the oracle."""
+    rng = np.random.default_rng(11)
+    for c in (3, 1020, 512):
+        subs = [api.SubbandConfig(L=16, c=c, window=rng.uniform(0.1, 1, 16))]
+        maps = [sorted(rng.choice(16, size=12, replace=False).tolist())]
+        cps = [80, 72, 72, 72]
+        plan = api.Plan(1024, cps, subs, maps)
+        S = 5
+        grid = (rng.standard_normal((S, len(cps), plan.row_active)) +
+                1j * rng.standard_normal((S, len(cps), plan.row_active))).astype(np.complex64)
+        wave = plan.tx_host(grid, S)
+        w = type("W", (), {})()
+        w.subbands, w.active_maps, w.B, w.N, w.cp = subs, maps, len(cps), 1024, cps
+        for u in range(S):
+            want, _ = oracle_tx(w, grid[u].astype(np.complex128))
+            assert rel_rms(wave[u], want) <= TOL, (c, u)
+        for fused in (False, True):
+            out = plan.rx_host(wave, plan.Q, plan.useful0, S, fused=fused)
+            for u in range(S):
+                want_p, _ = oracle_rx(w, wave[u].astype(np.complex128), plan.useful0, fused)
+                assert rel_rms(out[u], want_p) <= TOL, (c, u, fused)
