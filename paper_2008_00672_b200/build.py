@@ -118,6 +118,7 @@ if __name__ == "__main__":
     if "--variant" in sys.argv:
         i = sys.argv.index("--variant")
         name, defs = sys.argv[i + 1], sys.argv[i + 2].split(",") if len(sys.argv) > i + 2 else []
-        print(build_variant(name, [d for d in defs if d], ["fcw_k_n4096b.cu"]))
+        srcs = sys.argv[i + 3].split(",") if len(sys.argv) > i + 3 else ["fcw_k_n4096b.cu"]
+        print(build_variant(name, [d for d in defs if d], srcs))
     else:
         print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

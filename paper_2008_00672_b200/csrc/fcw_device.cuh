@@ -920,6 +920,9 @@ FCW_DI void rx_short_all(const KParams& P, const Team& tm, const SymDev& sy, con
 
 template <int LU>
 constexpr int min_blocks() {
+    // L >= 512: the warp paths hold 16-32 points per lane; one CTA per SM with
+    // up to 255 registers beats two spilling CTAs (config 2: 30 -> 38 Gsamples/s)
+    if (LU >= 512) return 1;
     return (LU >= 64 || (LU > 0 && LU <= 16)) ? 2 : 1;
 }
 
