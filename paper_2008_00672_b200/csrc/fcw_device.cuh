@@ -1060,6 +1060,18 @@ struct RunSource {
         }
     }
 
+    // Static mode: the (unit, symbol) the NEXT run starts at, or false.
+    FCW_DI bool peek(const KParams& P, int& unit, int& n0) const {
+        if constexpr (DYN) {
+            return false;
+        } else {
+            if (pos >= hi) return false;
+            unit = pos / P.B;
+            n0 = pos - unit * P.B;
+            return true;
+        }
+    }
+
     // Next run (unit, [n0, n1)); false when the team is done.
     FCW_DI bool next(const KParams& P, int* s_item, int g, int gtid, int nthr, int& unit, int& n0, int& n1) {
         if constexpr (!DYN) {
@@ -1143,7 +1155,13 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) tx_kernel(const KP
         const float2* in_u = P.in + (long long)unit * P.in_stride;
         float2* out_u = P.out + (long long)unit * P.out_stride;
         const int nfirst = n0 > 0 ? n0 - 1 : 0;
-        if (gtid == 0) prefetch_l2(in_u + (long long)nfirst * P.row_len, 8LL * P.row_len);
+        if (gtid == 0) {
+            prefetch_l2(in_u + (long long)nfirst * P.row_len, 8LL * P.row_len);
+            int un, nn;  // static mode: the next run's first row is on its way too
+            if (runs.peek(P, un, nn))
+                prefetch_l2(P.in + (long long)un * P.in_stride + (long long)(nn > 0 ? nn - 1 : 0) * P.row_len,
+                            8LL * P.row_len);
+        }
 
         for (int n = nfirst; n < n1; ++n) {
             const SymDev sy = P.sym[n];
@@ -1255,7 +1273,12 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) rx_kernel(const KP
     while (runs.next(P, S.s_item, g, gtid, TT, unit, n0, n1)) {
         const float2* in_u = P.in + (long long)unit * P.in_stride;
         float2* out_u = P.out + (long long)unit * P.out_stride;
-        if (gtid == 0) prefetch_l2(in_u + P.rx_base + P.sym[n0].sigma, 8LL * (3 * N / 2));
+        if (gtid == 0) {
+            prefetch_l2(in_u + P.rx_base + P.sym[n0].sigma, 8LL * (3 * N / 2));
+            int un, nn;  // static mode: the next run's first window is on its way too
+            if (runs.peek(P, un, nn))
+                prefetch_l2(P.in + (long long)un * P.in_stride + P.rx_base + P.sym[nn].sigma, 8LL * (3 * N / 2));
+        }
 
         for (int n = n0; n < n1; ++n) {
             const SymDev sy = P.sym[n];
