@@ -461,6 +461,100 @@ constexpr int teams_per_cta() {
     return (N >= 512 && N <= 4096) ? 4096 / N : 1;
 }
 
+// ------------------------------------------ L = 16 on 16-lane groups (C1)
+// Narrowband plans (ZV = 2) have at most a handful of L = 16 subbands per
+// team; one thread per subband leaves the team waiting on a 3-transform chain.
+// Here each subband gets a 16-lane group, one bin per lane, and the 16-point
+// transforms run across the lanes (radix-2 DIF by xor shuffles, then one
+// bit-reversal shuffle).  Lane b of group i: bin b of subband i.
+
+// X[b] of the 16 values held by the group's lanes (natural order in and out);
+// SIGN = -1 forward, +1 inverse (unscaled).  tw = plan table exp(-2 pi i m / N).
+template <int N, int SIGN, int NV>
+FCW_DI void lane_fft16(float2 (&v)[NV], int b, const float2* __restrict__ tw) {
+#pragma unroll
+    for (int h = 8; h >= 1; h >>= 1) {
+        const bool up = b & h;
+        float2 w = __ldg(&tw[(b & (h - 1)) * (8 / h) * (N / 16)]);
+        if (SIGN > 0) w.y = -w.y;
+#pragma unroll
+        for (int f = 0; f < NV; ++f) {
+            float2 o;
+            o.x = __shfl_xor_sync(0xffffffffu, v[f].x, h);
+            o.y = __shfl_xor_sync(0xffffffffu, v[f].y, h);
+            v[f] = up ? cmul(csub(o, v[f]), w) : cadd(v[f], o);
+        }
+    }
+    const int src = (threadIdx.x & ~15) | (int)(__brev((unsigned)b) >> 28);  // X[b] sits in lane brev4(b)
+#pragma unroll
+    for (int f = 0; f < NV; ++f) {
+        v[f].x = __shfl_sync(0xffffffffu, v[f].x, src & 31);
+        v[f].y = __shfl_sync(0xffffffffu, v[f].y, src & 31);
+    }
+}
+
+template <int N>
+FCW_DI void tx_short_lanes16(const KParams& P, const Team& tm, const SymDev& sy, const float2* __restrict__ row,
+                             float2* spec0, float2* spec1) {
+    constexpr int L = 16;
+    const int b = tm.tid & 15;
+    for (int i0 = (tm.tid >> 5) * 2; i0 < P.M; i0 += tm.nthr / 16) {  // warp-uniform: two groups per warp
+        const int i = i0 + ((tm.tid >> 4) & 1);
+        const bool act = i < P.M;
+        const SubDev sd = P.sub[act ? i : i0];
+        const Bin e = bin_entry<N, L>(P, sd, b);
+        const float2 ph = cscale(tw_conj(P.tw, theta_exp<N>(sd.cmodN, sy.smodN)), sd.tx_scale);
+        float2 x[1] = {act ? cmul(grid_val(P, sd, row, b, e.inv), ph) : zero2()};
+        lane_fft16<N, +1, 1>(x, b, P.tw);  // ofdm_modulate (scale folded into ph)
+        const int lcp = sy.cp >> sd.logI;
+        // block windows of tx_symbol (fc_sync.cpp:34-84): element b of block 0 is
+        // x[(b - L/4) mod L] on [L/4 - l_cp, 3L/4), of block 1 x[b + L/4] on [L/4, 3L/4)
+        const int base = threadIdx.x & ~15;
+        float2 u[2];
+        u[0].x = __shfl_sync(0xffffffffu, x[0].x, (base | ((b - 4) & 15)) & 31);
+        u[0].y = __shfl_sync(0xffffffffu, x[0].y, (base | ((b - 4) & 15)) & 31);
+        u[1].x = __shfl_sync(0xffffffffu, x[0].x, (base | ((b + 4) & 15)) & 31);
+        u[1].y = __shfl_sync(0xffffffffu, x[0].y, (base | ((b + 4) & 15)) & 31);
+        if (!((b >= L / 4 - lcp) && (b < 3 * L / 4))) u[0] = zero2();
+        if (!((b >= L / 4) && (b < 3 * L / 4))) u[1] = zero2();
+        lane_fft16<N, -1, 2>(u, b, P.tw);
+        if (act && e.dest >= 0) {
+            spec0[e.dest] = cscale(u[0], e.w);
+            spec1[e.dest] = cscale(u[1], e.w * sd.bp1);
+        }
+    }
+}
+
+// Fused RX (Eq. 30, fc_sync.cpp:195-243) on 16-lane groups, as rx_short_thread.
+template <int N>
+FCW_DI void rx_short_lanes16(const KParams& P, const Team& tm, const SymDev& sy, const float2* spec0,
+                             const float2* spec1, float2* __restrict__ orow) {
+    constexpr int L = 16;
+    const int b = tm.tid & 15;
+    for (int i0 = (tm.tid >> 5) * 2; i0 < P.M; i0 += tm.nthr / 16) {
+        const int i = i0 + ((tm.tid >> 4) & 1);
+        const bool act = i < P.M;
+        const SubDev sd = P.sub[act ? i : i0];
+        const Bin e = bin_entry<N, L>(P, sd, b);
+        const int q = (sd.c - L / 2 + (b ^ (L / 2))) & (N - 1);
+        const float2 g0 = cscale(spec0[q], e.w);
+        float2 t = cscale(spec1[q], e.w * sd.bp1);
+        if (b & 1) t = make_float2(-t.x, -t.y);           // t = Omega_{L/2} g1
+        float2 f[1] = {mul_jpow_rt(csub(g0, t), b & 3)};  // f = Omega_{-L/4}(g0 - t)
+        lane_fft16<N, +1, 1>(f, b, P.tw);
+        if (b >= L / 2) f[0] = zero2();                   // S-hat
+        lane_fft16<N, -1, 1>(f, b, P.tw);
+        const float2 ph = __ldg(&P.tw[theta_exp<N>(sd.cmodN, sy.smodN)]);  // conj(theta_n)
+        const float a = sd.rx_s0 / (float)L, s = sd.rx_s0;
+        const float2 tj = mul_jpow_rt(t, b & 3);
+        const float2 o = cmul(make_float2(fmaf(f[0].x, a, tj.x * s), fmaf(f[0].y, a, tj.y * s)), ph);
+        if (act) {
+            if (P.grid_full) orow[sd.full_off + b] = o;
+            else if (e.inv >= 0) orow[sd.act_off + e.inv] = o;
+        }
+    }
+}
+
 // ----------------------------------------------- team-wide short transforms
 // For few large subbands (M <= warps/2, L >= 512: config 3's single L = 1024 /
 // L = 512 banks) one warp per subband would leave the team's other warps
@@ -598,7 +692,9 @@ template <int N, int LU, int ZV = 0>
 FCW_DI void tx_short_all(const KParams& P, const Team& tm, const SymDev& sy, const float2* __restrict__ row,
                          const float2* __restrict__ row_next, bool staged, float2* spec0, float2* spec1,
                          float2* scr, const float2* stw) {
-    if constexpr (use_team_short<N, LU>()) {
+    if constexpr (ZV == 2 && LU == 16) {
+        tx_short_lanes16<N>(P, tm, sy, row, spec0, spec1);
+    } else if constexpr (use_team_short<N, LU>()) {
         // few subbands: the whole team per subband; else one warp per subband
         if (2 * P.M <= tm.nwarp)
             tx_short_team<N, LU, teams_per_cta<N>()>(P, tm, sy, row, spec0, spec1, scr);
@@ -890,7 +986,12 @@ FCW_DI void rx_short_one(const KParams& P, const Team& tm, const SymDev& sy, con
 template <int N, int LU, int ZV = 0>
 FCW_DI void rx_short_all(const KParams& P, const Team& tm, const SymDev& sy, const float2* spec0,
                          const float2* spec1, float2* orow, float2* scr, const float2* stw) {
-    if constexpr (use_team_short<N, LU>()) {
+    if constexpr (ZV == 2 && LU == 16) {
+        if (P.fused)
+            rx_short_lanes16<N>(P, tm, sy, spec0, spec1, orow);
+        else
+            rx_short_one<N, LU>(P, tm, sy, spec0, spec1, orow, scr, stw, 0, P.M);
+    } else if constexpr (use_team_short<N, LU>()) {
         if (2 * P.M > tm.nwarp)
             rx_short_one<N, LU>(P, tm, sy, spec0, spec1, orow, scr, stw, 0, P.M);
         else if (P.fused)
