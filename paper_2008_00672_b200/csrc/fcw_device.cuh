@@ -1267,7 +1267,11 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) tx_kernel(const KP
         for (int n = nfirst; n < n1; ++n) {
             const SymDev sy = P.sym[n];
             team_sync<G>(g, TT);  // previous symbol's transform no longer reads spec
-            if (gtid == 0 && n + 1 < n1) prefetch_l2(in_u + (long long)(n + 1) * P.row_len, 8LL * P.row_len);
+            if (gtid == 0 && n + 1 < n1) {
+                prefetch_l2(in_u + (long long)(n + 1) * P.row_len, 8LL * P.row_len);
+                // FCW_TX_ACCUMULATE reads the waveform it adds to: bring the next symbol's span in too
+                if (P.accumulate) prefetch_l2(out_u + P.sym[n + 1].sigma, 8LL * (3 * N / 2));
+            }
             if (!(P.dbg_skip & 1))
                 tx_short_all<N, LU, ZV>(P, tm, sy, in_u + (long long)n * P.row_len,
                                     n + 1 < n1 ? in_u + (long long)(n + 1) * P.row_len : nullptr, n > nfirst,
