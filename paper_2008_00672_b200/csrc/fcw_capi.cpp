@@ -106,9 +106,58 @@ namespace fcw {
 // shared with the other C-ABI translation units (fcw_cont.cu)
 int set_error(int code, const std::string& msg) { return fail(code, msg); }
 int set_cuda_error(cudaError_t e, const char* where) { return cuda_fail(e, where); }
+
 }  // namespace fcw
 
 struct fcw_plan : fcw::Plan {};
+
+namespace fcw {
+// Continuous FC with time-domain I/O (fcw_cont.cu): the fused kernels read
+// the subband streams (TX) or write the output streams (RX) through the
+// column descriptors td, instead of a full grid that cont_cols_kernel
+// transforms.  p is a cp = 0 plan whose short paths support it (see
+// fcw_cont_plan_create).
+int tx_time_domain(const fcw_plan* p, const fc_col* td, const float2* streams, long long stream_stride,
+                   float2* wave, long long wave_stride, int S, cudaStream_t st) {
+    KParams kp{};
+    fill_common(*p, kp);
+    if ((long long)S * p->B >= (1LL << 31)) return fail(FCW_ENOTSUP, "S*B symbols per launch must be < 2^31");
+    pick_schedule(*p, S, true, kp);
+    kp.row_len = 0;
+    kp.grid_full = 1;
+    kp.td = td;
+    kp.in = streams;
+    kp.in_stride = stream_stride;
+    kp.out = wave;
+    kp.out_stride = wave_stride;
+    const cudaError_t e = launch_tx(*p, kp, S, st);
+    return e == cudaSuccess ? FCW_OK : cuda_fail(e, "continuous tx launch");
+}
+
+// RX input is the caller's waveform itself: the kernel reads it at
+// rx_base + sigma_n with zeros outside [0, wave_len) (rx_base = -N_L: the
+// N_L zeros rx_continuous prepends, fc_core.cpp:207-208).
+int rx_time_domain(const fcw_plan* p, const fc_col* td, const float2* wave, long long wave_stride,
+                   long long wave_len, long long rx_base, float2* out, long long out_stride, int S,
+                   cudaStream_t st) {
+    KParams kp{};
+    fill_common(*p, kp);
+    if ((long long)S * p->B >= (1LL << 31)) return fail(FCW_ENOTSUP, "S*B symbols per launch must be < 2^31");
+    pick_schedule(*p, S, false, kp);
+    kp.row_len = 0;
+    kp.grid_full = 1;
+    kp.fused = 0;
+    kp.td = td;
+    kp.rx_base = rx_base;
+    kp.wave_len = wave_len;
+    kp.in = wave;
+    kp.in_stride = wave_stride;
+    kp.out = out;
+    kp.out_stride = out_stride;
+    const cudaError_t e = launch_rx(*p, kp, S, st);
+    return e == cudaSuccess ? FCW_OK : cuda_fail(e, "continuous rx launch");
+}
+}  // namespace fcw
 
 extern "C" {
 

@@ -18,10 +18,17 @@
 //        out[R L_S + u] = sqrt(I) z_R[L_L + u] for R = 2n, 2n+1.
 // The waveform is zero-extended by N_L in front for RX, as rx_continuous
 // does (fc_core.cpp:207-208).
+// Where the kernels' short paths support it (TX: uniform L = 256; RX: every
+// L <= 256) the column passes cancel against the kernels' own short IDFT
+// (TX) / OFDM DFT (RX), so the kernels run with time-domain I/O instead
+// (KParams.td, fcw::tx_time_domain / rx_time_domain): no column passes, no
+// grid round trip, no RX staging copy (RX reads the waveform with zeros
+// outside it).
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -43,6 +50,11 @@ struct fcw_cont_plan {
     fcw::fc_col* d_cols = nullptr;  // per-subband column descriptors
     float2* d_tw = nullptr;         // exp(-2 pi i k / Lmax)
     int row_full = 0;
+    // time-domain I/O of the fused kernels (no column passes, no grid round
+    // trip, no RX staging copy) where their short paths support it:
+    // TX: uniform L = 256 (half-warp path); RX: every L <= 256 (warp and
+    // thread direct paths).  FCW_CONT_COLUMNS=1 forces the column passes.
+    bool td_tx = false, td_rx = false;
 };
 
 namespace fcw {
@@ -278,6 +290,17 @@ int fcw_cont_plan_create(fcw_cont_plan** out, int N, double overlap, const fcw_s
     p->row_full = ti.row_full;
     // RX input: N_L zeros, the waveform, zeros up to the last block pair
     p->rx_pad_len = std::max<int64_t>(ri.Q, prm[0].N_L + rx_wave_len);
+    {
+        const char* e = std::getenv("FCW_CONT_COLUMNS");
+        const bool cols = e && std::atoi(e) != 0;
+        bool u256 = N >= 256, le256 = true;
+        for (int m = 0; m < M; ++m) {
+            u256 = u256 && sbs[m].L == 256;
+            le256 = le256 && sbs[m].L <= 256;
+        }
+        p->td_tx = !cols && u256;
+        p->td_rx = !cols && le256;
+    }
     int off = 0;
     for (int m = 0; m < M; ++m) {
         fcw::fc_col c{};
@@ -354,6 +377,9 @@ int fcw_tx_continuous(const fcw_cont_plan* p, const void* streams, void* wave, i
     if (S == 0) return FCW_OK;
     if (!streams || !wave) return fcw::set_error(FCW_EINVAL, "null buffer");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (p->td_tx)
+        return fcw::tx_time_domain(p->tx, p->d_cols, static_cast<const float2*>(streams), p->stream_total,
+                                   static_cast<float2*>(wave), p->tx_Q, S, st);
     const long long grid_stride = (long long)p->B_tx * p->row_full;
     float2* grid = nullptr;
     cudaError_t e = fcw::scratch_alloc(&grid, sizeof(float2) * grid_stride * S, st);
@@ -380,6 +406,10 @@ int fcw_rx_continuous(const fcw_cont_plan* p, const void* wave, void* out, int S
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     fcw_plan_info ri{};
     fcw_plan_get_info(p->rx, &ri);
+    if (p->td_rx)
+        return fcw::rx_time_domain(p->rx, p->d_cols, static_cast<const float2*>(wave), p->rx_wave_len,
+                                   p->rx_wave_len, -(long long)ri.N_L, static_cast<float2*>(out), p->rx_out_total,
+                                   S, st);
     const long long grid_stride = (long long)p->B_rx * p->row_full;
     const long long pad = p->rx_pad_len;
     float2 *wp = nullptr, *grid = nullptr;

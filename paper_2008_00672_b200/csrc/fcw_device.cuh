@@ -373,6 +373,22 @@ FCW_DI void tx_short_half(const KParams& P, const Team& tm, const SymDev& sy, co
         const SubDev sd = P.sub[m];
         const int2* ce = P.cls + sd.cls_off + t;
         float2 v[PPT];
+        bool td = false;  // time-domain input (continuous FC): x itself, no IDFT
+        if constexpr (ZV == 0) td = P.td != nullptr;
+        if (td) {
+            // block pair n carries x = stream[n L - L_T, + L), zero outside the
+            // stream (cont_cols_kernel's DFT / sqrt(L) and this IDFT cancel:
+            // v = sqrt(L) ph x)
+            const fc_col d = P.td[m];
+            const long long j0 = (sy.sigma / N) * L - d.lt + t;
+            const float2 ph = cscale(tw_conj(P.tw, theta_exp<N>(sd.cmodN, sy.smodN)), sd.tx_scale * 16.f);
+            const float2* x = row + d.in_off;
+#pragma unroll
+            for (int k = 0; k < PPT; ++k) {
+                const long long j = j0 + TW * k;
+                v[k] = (act && j >= 0 && j < d.len) ? cmul(ld_stream(x + j), ph) : zero2();
+            }
+        } else {
         {
             const float2 ph = cscale(tw_conj(P.tw, theta_exp<N>(sd.cmodN, sy.smodN)), sd.tx_scale);
             constexpr unsigned long long ZI = ZV == 1 ? kZ6 : 0ull;
@@ -400,6 +416,7 @@ FCW_DI void tx_short_half(const KParams& P, const Team& tm, const SymDev& sy, co
                 if (live(k)) v[k] = cmul(v[k], ph);
         }
         fft256_half<+1, ZV == 1 ? kZ6 : 0ull>(v, buf, stw, t, 0, tw16_of(P, stw));  // x[t + 16 m] (scales in ph)
+        }
         const int lcp = sy.cp >> sd.logI;
         const int qbase = sd.c - L / 2 + t, ext0 = N + sd.ext_base;
         const int r0 = pair ? 0 : h, r1 = pair ? 2 : h + 1;
@@ -724,7 +741,7 @@ FCW_DI void tx_short_all(const KParams& P, const Team& tm, const SymDev& sy, con
 
 // ---------------------------------------------------------------- K-RX parts
 
-template <int N, int L>
+template <int N, int L, bool TDIO = true>  // TDIO: time-domain output compiled in (continuous FC)
 FCW_DI void rx_short_thread(const KParams& P, const Team& tm, const SymDev& sy, const float2* spec0,
                             const float2* spec1, float2* __restrict__ orow, int gstart, int gcount) {
     for (int i = tm.tid; i < gcount; i += tm.nthr) {
@@ -781,6 +798,16 @@ FCW_DI void rx_short_thread(const KParams& P, const Team& tm, const SymDev& sy, 
                 x[k] = g0[L / 4 + k];
                 x[L / 2 + k] = g1[L / 4 + k];
             }
+            if (TDIO && P.td) {  // time-domain output (continuous FC), as rx_short_warp
+                const fc_col d = P.td[m];
+                const long long base = (sy.sigma / N) * L;
+                const float2 phs = cscale(ph, sd.rx_s0 * rsqrtf((float)L));
+                float2* o = orow + d.out_off;
+#pragma unroll
+                for (int b = 0; b < L; ++b)
+                    if (base + b < d.len_out) o[base + b] = cmul(x[b], phs);
+                continue;
+            }
             fft_reg<L, -1>(x);
             const float2 phs = cscale(ph, sd.rx_s0 / (float)L);
 #pragma unroll
@@ -798,7 +825,7 @@ FCW_DI void rx_short_thread(const KParams& P, const Team& tm, const SymDev& sy, 
     }
 }
 
-template <int N, int L>
+template <int N, int L, bool TDIO = true>  // TDIO: time-domain output compiled in (continuous FC)
 FCW_DI void rx_short_warp(const KParams& P, const Team& tm, const SymDev& sy, const float2* spec0,
                           const float2* spec1, float2* __restrict__ orow, float2* scr, const float2* stw, int gstart,
                           int gcount) {
@@ -867,6 +894,22 @@ FCW_DI void rx_short_warp(const KParams& P, const Team& tm, const SymDev& sy, co
                     const int e = lane + 32 * k;
                     x[0][k] = (k < PPT / 2) ? scr[L / 4 + e] : s1[L / 4 + e - L / 2];
                 }
+            }
+            if (TDIO && P.td) {
+                // time-domain output (continuous FC): x itself, no OFDM DFT
+                // (cont_cols_kernel's IDFT / sqrt(L) would undo it): pair n
+                // lands at out[n L, + L) of subband m's output stream
+                const fc_col d = P.td[m];
+                const long long base = (sy.sigma / N) * L;
+                const float2 phs = cscale(ph, sd.rx_s0 * rsqrtf((float)L));
+                float2* o = orow + d.out_off;
+#pragma unroll
+                for (int k = 0; k < PPT; ++k) {
+                    const long long j = base + lane + 32 * k;
+                    if (j < d.len_out) o[j] = cmul(x[0][k], phs);
+                }
+                __syncwarp();
+                continue;
             }
             team_fft<L, 32, PPT, -1, 1, false>(x, b1, stw, sts, lane, true);
             const float2 phs = cscale(ph, sd.rx_s0 / (float)L);
@@ -972,14 +1015,14 @@ FCW_DI void rx_short_one(const KParams& P, const Team& tm, const SymDev& sy, con
                          const float2* spec1, float2* orow, float2* scr, const float2* stw, int gs, int gc) {
     if constexpr (L <= N) {
         if constexpr (L <= 32)
-            rx_short_thread<N, L>(P, tm, sy, spec0, spec1, orow, gs, gc);
+            rx_short_thread<N, L, ZV != 1>(P, tm, sy, spec0, spec1, orow, gs, gc);
         else if constexpr (L == 256 && MIRROR) {
             if (P.fused)
                 rx_short_half<N, L, ZV>(P, tm, sy, spec0, spec1, orow, scr, stw, gs, gc);
             else
-                rx_short_warp<N, L>(P, tm, sy, spec0, spec1, orow, scr, stw, gs, gc);
+                rx_short_warp<N, L, ZV != 1>(P, tm, sy, spec0, spec1, orow, scr, stw, gs, gc);
         } else
-            rx_short_warp<N, L>(P, tm, sy, spec0, spec1, orow, scr, stw, gs, gc);
+            rx_short_warp<N, L, ZV != 1>(P, tm, sy, spec0, spec1, orow, scr, stw, gs, gc);
     }
 }
 
@@ -1389,7 +1432,18 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) rx_kernel(const KP
             const SymDev sy = P.sym[n];
             if (gtid == 0 && n + 1 < n1) prefetch_l2(in_u + P.rx_base + P.sym[n + 1].sigma, 8LL * (3 * N / 2));
             float2 v[2][kPPT];
-            if (act) {
+            bool bounded = false;  // continuous FC: zeros outside [0, wave_len) (rx_continuous pads)
+            if constexpr (ZV == 0) bounded = P.td != nullptr;
+            if (act && bounded) {
+                const long long j0 = P.rx_base + sy.sigma + gtid;
+#pragma unroll
+                for (int mm = 0; mm < 24; ++mm) {
+                    const long long j = j0 + T * mm;
+                    const float2 val = (j >= 0 && j < P.wave_len) ? ld_stream(in_u + j) : zero2();
+                    if (mm < 16) v[0][mm] = val;
+                    if (mm >= 8) v[1][mm - 8] = val;
+                }
+            } else if (act) {
                 // rx_segment (fc_sync.cpp:145-156): y0 = w[start, +N), y1 = w[start + N/2, +N)
                 const float2* src = in_u + P.rx_base + sy.sigma + gtid;
 #pragma unroll

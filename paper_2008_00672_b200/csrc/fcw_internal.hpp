@@ -45,6 +45,8 @@ struct SymDev {
     int pad_[2];
 };
 
+struct fc_col;  // continuous-FC column descriptor (below)
+
 // Kernel parameter block (passed by value).
 struct KParams {
     int N, B, M;
@@ -81,6 +83,10 @@ struct KParams {
     const int* fix_slot; // [n_ext] its extension slot
     const int* zero_list;  // [n_zero] bins no subband touches
     const float2* tw;    // [N] exp(-2 pi i k / N)
+    // time-domain I/O of the continuous FC (fcw_cont.cu, cp = 0 plans; null =
+    // grid I/O): TX reads each subband's low-rate stream, RX writes each
+    // subband's output stream, per subband m at td[m] offsets, pair n = sigma / N
+    const fc_col* td;
     const float2* in;
     float2* out;
     int* item_counter;   // per-launch scratch: dynamic run counter
@@ -182,5 +188,11 @@ cudaError_t psd(const float2* wave, long long stride, long long len, int S, int 
                 cudaStream_t st);
 size_t rx_smem_bytes(const Plan& plan);
 void fill_common(const Plan& plan, KParams& kp);
+// fcw_capi.cpp: continuous FC with time-domain I/O (fcw_cont.cu)
+int tx_time_domain(const fcw_plan* p, const fc_col* td, const float2* streams, long long stream_stride,
+                   float2* wave, long long wave_stride, int S, cudaStream_t st);
+int rx_time_domain(const fcw_plan* p, const fc_col* td, const float2* wave, long long wave_stride,
+                   long long wave_len, long long rx_base, float2* out, long long out_stride, int S,
+                   cudaStream_t st);
 
 }  // namespace fcw

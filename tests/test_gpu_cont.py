@@ -21,11 +21,17 @@ CASES = [
     (1024, [16, 64, 256], [500, 200, 900], [230, 64, 513]),
     (2048, [512, 1024], [300, 1500], [1000, 2001]),
     (4096, [256] * 3, [3000, 3300, 3600], [2000, 2000, 1999]),
+    (1024, [256, 256], [200, 700], [100, 257]),
 ]
 
 
+@pytest.mark.parametrize("columns", [0, 1], ids=["time_domain_io", "column_passes"])
 @pytest.mark.parametrize("N,Ls,cs,lens", CASES)
-def test_continuous_tx_rx_match_oracle(N, Ls, cs, lens):
+def test_continuous_tx_rx_match_oracle(N, Ls, cs, lens, columns, monkeypatch):
+    # FCW_CONT_COLUMNS=1 forces the DFT_L / IDFT_L column passes around the
+    # grid-I/O kernels; by default plans whose short paths support it run the
+    # fused kernels with time-domain I/O (TX: uniform L = 256, RX: L <= 256)
+    monkeypatch.setenv("FCW_CONT_COLUMNS", str(columns))
     rng = np.random.default_rng(N + len(Ls))
     wins = [rng.uniform(0, 1, L) for L in Ls]
     subs = [api.SubbandConfig(L=L, c=c, window=w) for L, c, w in zip(Ls, cs, wins)]
