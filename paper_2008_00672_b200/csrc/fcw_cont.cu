@@ -18,9 +18,9 @@
 //        out[R L_S + u] = sqrt(I) z_R[L_L + u] for R = 2n, 2n+1.
 // The waveform is zero-extended by N_L in front for RX, as rx_continuous
 // does (fc_core.cpp:207-208).
-// Where the kernels' short paths support it (TX: uniform L = 256; RX: every
-// L <= 256) the column passes cancel against the kernels' own short IDFT
-// (TX) / OFDM DFT (RX), so the kernels run with time-domain I/O instead
+// Where the kernels' short paths support it (every L <= 256) the column
+// passes cancel against the kernels' own short IDFT (TX) / OFDM DFT (RX), so
+// the kernels run with time-domain I/O instead
 // (KParams.td, fcw::tx_time_domain / rx_time_domain): no column passes, no
 // grid round trip, no RX staging copy (RX reads the waveform with zeros
 // outside it).
@@ -51,9 +51,10 @@ struct fcw_cont_plan {
     float2* d_tw = nullptr;         // exp(-2 pi i k / Lmax)
     int row_full = 0;
     // time-domain I/O of the fused kernels (no column passes, no grid round
-    // trip, no RX staging copy) where their short paths support it:
-    // TX: uniform L = 256 (half-warp path); RX: every L <= 256 (warp and
-    // thread direct paths).  FCW_CONT_COLUMNS=1 forces the column passes.
+    // trip, no RX staging copy) where their short paths support it: L <= 256
+    // (TX thread path in mixed-L plans only, warp-lockstep and half-warp
+    // paths; RX thread / warp direct paths).  FCW_CONT_COLUMNS=1 forces the
+    // column passes.
     bool td_tx = false, td_rx = false;
 };
 
@@ -293,12 +294,14 @@ int fcw_cont_plan_create(fcw_cont_plan** out, int N, double overlap, const fcw_s
     {
         const char* e = std::getenv("FCW_CONT_COLUMNS");
         const bool cols = e && std::atoi(e) != 0;
-        bool u256 = N >= 256, le256 = true;
+        bool le256 = true, uni = true;
         for (int m = 0; m < M; ++m) {
-            u256 = u256 && sbs[m].L == 256;
             le256 = le256 && sbs[m].L <= 256;
+            uni = uni && sbs[m].L == sbs[0].L;
         }
-        p->td_tx = !cols && u256;
+        // TX: the thread (L <= 32, mixed-L plans only), warp-lockstep
+        // (64 <= L <= 256) and half-warp (uniform L = 256) paths
+        p->td_tx = !cols && le256 && !(uni && sbs[0].L <= 32);
         p->td_rx = !cols && le256;
     }
     int off = 0;

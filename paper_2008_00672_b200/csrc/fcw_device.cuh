@@ -139,7 +139,7 @@ struct Team {
 // ---------------------------------------------------------------- K-TX parts
 
 // Short-side TX of one subband-symbol by one thread (L <= 32).
-template <int N, int L>
+template <int N, int L, bool TDIO = true>  // TDIO: time-domain input compiled in (continuous FC)
 FCW_DI void tx_short_thread(const KParams& P, const Team& tm, const SymDev& sy, const float2* __restrict__ row,
                             float2* spec0, float2* spec1, int gstart, int gcount) {
     for (int i = tm.tid; i < gcount; i += tm.nthr) {
@@ -147,9 +147,19 @@ FCW_DI void tx_short_thread(const KParams& P, const Team& tm, const SymDev& sy, 
         const SubDev sd = P.sub[m];
         float2 x[L];
         const float2 ph = cscale(tw_conj(P.tw, theta_exp<N>(sd.cmodN, sy.smodN)), sd.tx_scale);
+        if (TDIO && P.td) {
+            // time-domain input (continuous FC, as tx_short_half): x = sqrt(L) ph stream[n L - L_T + b]
+            const fc_col d = P.td[m];
+            const long long j0 = (sy.sigma / N) * L - d.lt;
+            const float2 phs = cscale(ph, sqrtf((float)L));
 #pragma unroll
-        for (int b = 0; b < L; ++b) x[b] = cmul(grid_val(P, sd, row, b, bin_entry<N, L>(P, sd, b).inv), ph);
-        fft_reg<L, +1>(x);  // ofdm_modulate (scale folded into ph)
+            for (int b = 0; b < L; ++b)
+                x[b] = (j0 + b >= 0 && j0 + b < d.len) ? cmul(row[d.in_off + j0 + b], phs) : zero2();
+        } else {
+#pragma unroll
+            for (int b = 0; b < L; ++b) x[b] = cmul(grid_val(P, sd, row, b, bin_entry<N, L>(P, sd, b).inv), ph);
+            fft_reg<L, +1>(x);  // ofdm_modulate (scale folded into ph)
+        }
         const int lcp = sy.cp >> sd.logI;  // cp_truncate (fc_sync.cpp:26-32)
         float2 u0[L], u1[L];
 #pragma unroll
@@ -193,6 +203,17 @@ FCW_DI void tx_short_warp_lockstep(const KParams& P, const Team& tm, const SymDe
 #pragma unroll
         for (int k = 0; k < PPT; ++k) ent[k] = __ldg(&ce[32 * k]);
         float2 v[1][PPT];
+        if (P.td) {
+            // time-domain input (continuous FC, as tx_short_half): element lane + 32k of x
+            const fc_col d = P.td[m];
+            const long long j0 = (sy.sigma / N) * L - d.lt + lane;
+            const float2 phs = cscale(ph, sqrtf((float)L));
+#pragma unroll
+            for (int k = 0; k < PPT; ++k) {
+                const long long j = j0 + 32 * k;
+                v[0][k] = (j >= 0 && j < d.len) ? cmul(ld_stream(row + d.in_off + j), phs) : zero2();
+            }
+        } else {
         if (P.grid_full) {
             const float2* g = row + sd.full_off + lane;
 #pragma unroll
@@ -205,6 +226,7 @@ FCW_DI void tx_short_warp_lockstep(const KParams& P, const Team& tm, const SymDe
             for (int k = 0; k < PPT; ++k) v[0][k] = (short)(ent[k].x & 0xffff) >= 0 ? cmul(v[0][k], ph) : zero2();
         }
         team_fft<L, 32, PPT, +1, 1, false>(v, b1, stw, sts, lane, true);
+        }
         const int lcp = sy.cp >> sd.logI;
         float2 uu[2][PPT];  // block-0 / block-1 DFT inputs
         if constexpr (L >= 128) {
@@ -454,13 +476,15 @@ FCW_DI void tx_short_half(const KParams& P, const Team& tm, const SymDev& sy, co
 
 // HALF: the kernel carries the half-warp twiddle table (the uniform L = 256
 // specialisation); generic kernels use the whole-warp lockstep path.
-template <int N, int L, bool HALF = false, int ZV = 0>
+// TDT: the thread path carries the time-domain input (kept out of the
+// uniform L <= 32 kernels, where it measured +7% TX time on config 4)
+template <int N, int L, bool HALF = false, int ZV = 0, bool TDT = true>
 FCW_DI void tx_short_one(const KParams& P, const Team& tm, const SymDev& sy, const float2* __restrict__ row,
                          const float2* __restrict__ row_next, bool staged, float2* spec0, float2* spec1,
                          float2* scr, const float2* stw, int gs, int gc) {
     if constexpr (L <= N) {
         if constexpr (L <= 32)
-            tx_short_thread<N, L>(P, tm, sy, row, spec0, spec1, gs, gc);
+            tx_short_thread<N, L, TDT>(P, tm, sy, row, spec0, spec1, gs, gc);
         else if constexpr (L == 256 && HALF)
             tx_short_half<N, L, ZV>(P, tm, sy, row, spec0, spec1, scr, stw, gs, gc);
         else if constexpr (L <= 256)
@@ -719,7 +743,8 @@ FCW_DI void tx_short_all(const KParams& P, const Team& tm, const SymDev& sy, con
             tx_short_one<N, LU>(P, tm, sy, row, row_next, staged, spec0, spec1, scr, stw, 0, P.M);
     } else if constexpr (LU > 0) {
         // uniform L: the next symbol's first subband is staged across calls
-        tx_short_one<N, LU, LU == 256, ZV>(P, tm, sy, row, row_next, staged, spec0, spec1, scr, stw, 0, P.M);
+        tx_short_one<N, LU, LU == 256, ZV, (LU > 32)>(P, tm, sy, row, row_next, staged, spec0, spec1, scr, stw, 0,
+                                                   P.M);
     } else {
         for (int g = 0; g < P.n_groups; ++g) {
             const int gs = P.grp_start[g], gc = P.grp_count[g];
