@@ -112,6 +112,8 @@ int set_cuda_error(cudaError_t e, const char* where) { return cuda_fail(e, where
 struct fcw_plan : fcw::Plan {};
 
 namespace fcw {
+void plan_force_generic(fcw_plan* p) { p->generic = true; }
+
 // Continuous FC with time-domain I/O (fcw_cont.cu): the fused kernels read
 // the subband streams (TX) or write the output streams (RX) through the
 // column descriptors td, instead of a full grid that cont_cols_kernel

@@ -18,12 +18,11 @@
 //        out[R L_S + u] = sqrt(I) z_R[L_L + u] for R = 2n, 2n+1.
 // The waveform is zero-extended by N_L in front for RX, as rx_continuous
 // does (fc_core.cpp:207-208).
-// Where the kernels' short paths support it (every L <= 256) the column
-// passes cancel against the kernels' own short IDFT (TX) / OFDM DFT (RX), so
-// the kernels run with time-domain I/O instead
+// The column passes cancel against the kernels' own short IDFT (TX) / OFDM
+// DFT (RX), so by default the kernels run with time-domain I/O instead
 // (KParams.td, fcw::tx_time_domain / rx_time_domain): no column passes, no
 // grid round trip, no RX staging copy (RX reads the waveform with zeros
-// outside it).
+// outside it).  FCW_CONT_COLUMNS=1 keeps the column passes.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -51,10 +50,8 @@ struct fcw_cont_plan {
     float2* d_tw = nullptr;         // exp(-2 pi i k / Lmax)
     int row_full = 0;
     // time-domain I/O of the fused kernels (no column passes, no grid round
-    // trip, no RX staging copy) where their short paths support it: L <= 256
-    // (TX thread path in mixed-L plans only, warp-lockstep and half-warp
-    // paths; RX thread / warp direct paths).  FCW_CONT_COLUMNS=1 forces the
-    // column passes.
+    // trip, no RX staging copy).  FCW_CONT_COLUMNS=1 forces the column
+    // passes.
     bool td_tx = false, td_rx = false;
 };
 
@@ -294,15 +291,16 @@ int fcw_cont_plan_create(fcw_cont_plan** out, int N, double overlap, const fcw_s
     {
         const char* e = std::getenv("FCW_CONT_COLUMNS");
         const bool cols = e && std::atoi(e) != 0;
-        bool le256 = true, uni = true;
+        bool uni = true, big = false;
         for (int m = 0; m < M; ++m) {
-            le256 = le256 && sbs[m].L <= 256;
             uni = uni && sbs[m].L == sbs[0].L;
+            big = big || sbs[m].L >= 512;
         }
-        // TX: the thread (L <= 32, mixed-L plans only), warp-lockstep
-        // (64 <= L <= 256) and half-warp (uniform L = 256) paths
-        p->td_tx = !cols && le256 && !(uni && sbs[0].L <= 32);
-        p->td_rx = !cols && le256;
+        p->td_tx = !cols;
+        p->td_rx = !cols;
+        // the TX thread (L <= 32) and warp (L >= 512) paths carry the
+        // time-domain input in the generic kernels only (tx_short_one)
+        if (p->td_tx && (big || (uni && sbs[0].L <= 32))) fcw::plan_force_generic(p->tx);
     }
     int off = 0;
     for (int m = 0; m < M; ++m) {

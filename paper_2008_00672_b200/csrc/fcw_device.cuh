@@ -303,12 +303,31 @@ FCW_DI void stage_grid(const KParams& P, int m, const float2* __restrict__ row, 
     cp_async_commit();
 }
 
+// Time-domain input (continuous FC): request x = stream[n L - L_T + e],
+// e = lane + 32k, of subband m into the staging buffer (zero-filled outside
+// the stream).
+template <int N, int L>
+FCW_DI void stage_stream(const KParams& P, int m, const SymDev& sy, const float2* __restrict__ row, float2* stage,
+                         int lane) {
+    constexpr int PPT = L / 32;
+    const fc_col d = P.td[m];
+    const long long j0 = (sy.sigma / N) * L - d.lt + lane;
+    const float2* x = row + d.in_off;
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) {
+        const long long j = j0 + 32 * k;
+        const bool ok = j >= 0 && j < d.len;
+        cp_async8(&stage[lane + 32 * k], ok ? x + j : x, ok);
+    }
+    cp_async_commit();
+}
+
 // Short-side TX of one subband-symbol by one warp (L >= 64), lane holds bins
 // lane + 32k.  One padded scratch buffer per warp plus a staging buffer that
 // receives the NEXT subband's grid column by cp.async while this one is
 // transformed (the first subband of the next symbol when `row_next` is set;
 // `staged` says this symbol's first subband was requested that way).
-template <int N, int L>
+template <int N, int L, bool TDIO = true>  // TDIO: time-domain input compiled in (continuous FC)
 FCW_DI void tx_short_warp(const KParams& P, const Team& tm, const SymDev& sy, const float2* __restrict__ row,
                           const float2* __restrict__ row_next, bool staged, float2* spec0, float2* spec1,
                           float2* scr, const float2* stw, int gstart, int gcount) {
@@ -319,21 +338,31 @@ FCW_DI void tx_short_warp(const KParams& P, const Team& tm, const SymDev& sy, co
     float2* stage = scr + P.stage_off;
     auto sub_of = [&](int i) { return P.grp_sub ? __ldg(&P.grp_sub[gstart + i]) : gstart + i; };
     if (tm.warp >= gcount) return;
-    if (!staged) stage_grid<L>(P, sub_of(tm.warp), row, stage, lane);
+    // time-domain input (continuous FC): the stream column is staged instead
+    // of the grid column, within this symbol only (the caller passes no
+    // row_next), and the IDFT is skipped (as tx_short_half)
+    const bool td = TDIO && P.td != nullptr;
+    if (td) stage_stream<N, L>(P, sub_of(tm.warp), sy, row, stage, lane);
+    else if (!staged) stage_grid<L>(P, sub_of(tm.warp), row, stage, lane);
     for (int i = tm.warp; i < gcount; i += tm.nwarp) {
         const SubDev sd = P.sub[sub_of(i)];
-        const float2 ph = cscale(tw_conj(P.tw, theta_exp<N>(sd.cmodN, sy.smodN)), sd.tx_scale);
+        const float2 ph = cscale(tw_conj(P.tw, theta_exp<N>(sd.cmodN, sy.smodN)),
+                                 td ? sd.tx_scale * sqrtf((float)L) : sd.tx_scale);
         float2 v[1][PPT];
         cp_async_wait_all();
         __syncwarp();
 #pragma unroll
         for (int k = 0; k < PPT; ++k) v[0][k] = cmul(stage[lane + 32 * k], ph);
         __syncwarp();  // the staging buffer is free again
-        if (i + tm.nwarp < gcount)
-            stage_grid<L>(P, sub_of(i + tm.nwarp), row, stage, lane);
-        else if (row_next)
-            stage_grid<L>(P, sub_of(tm.warp), row_next, stage, lane);
-        team_fft<L, 32, PPT, +1, 1, false>(v, b1, stw, sts, lane, true);
+        if (td) {
+            if (i + tm.nwarp < gcount) stage_stream<N, L>(P, sub_of(i + tm.nwarp), sy, row, stage, lane);
+        } else {
+            if (i + tm.nwarp < gcount)
+                stage_grid<L>(P, sub_of(i + tm.nwarp), row, stage, lane);
+            else if (row_next)
+                stage_grid<L>(P, sub_of(tm.warp), row_next, stage, lane);
+            team_fft<L, 32, PPT, +1, 1, false>(v, b1, stw, sts, lane, true);
+        }
         const int lcp = sy.cp >> sd.logI;
         float2 uu[2][PPT];  // block-0 / block-1 DFT inputs (L/4 is a multiple of 32: register renames)
 #pragma unroll
@@ -476,8 +505,10 @@ FCW_DI void tx_short_half(const KParams& P, const Team& tm, const SymDev& sy, co
 
 // HALF: the kernel carries the half-warp twiddle table (the uniform L = 256
 // specialisation); generic kernels use the whole-warp lockstep path.
-// TDT: the thread path carries the time-domain input (kept out of the
-// uniform L <= 32 kernels, where it measured +7% TX time on config 4)
+// TDT: the thread and L >= 512 warp paths carry the time-domain input
+// (continuous FC).  Kept out of the uniform-L kernels, where it measured +7%
+// TX time on config 4 (L = 16) and +3% / +13% on configs 2 / 3 (L >= 512);
+// continuous plans with L >= 512 run the generic kernels (Plan::generic).
 template <int N, int L, bool HALF = false, int ZV = 0, bool TDT = true>
 FCW_DI void tx_short_one(const KParams& P, const Team& tm, const SymDev& sy, const float2* __restrict__ row,
                          const float2* __restrict__ row_next, bool staged, float2* spec0, float2* spec1,
@@ -490,7 +521,7 @@ FCW_DI void tx_short_one(const KParams& P, const Team& tm, const SymDev& sy, con
         else if constexpr (L <= 256)
             tx_short_warp_lockstep<N, L>(P, tm, sy, row, spec0, spec1, scr, stw, gs, gc);
         else
-            tx_short_warp<N, L>(P, tm, sy, row, row_next, staged, spec0, spec1, scr, stw, gs, gc);
+            tx_short_warp<N, L, TDT>(P, tm, sy, row, row_next, staged, spec0, spec1, scr, stw, gs, gc);
     }
 }
 
@@ -704,6 +735,17 @@ FCW_DI void rx_short_team(const KParams& P, const Team& tm, const SymDev& sy, co
 #pragma unroll
             for (int k = 0; k < PPT; ++k)
                 g0[0][k] = k < PPT / 2 ? gg[0][k + PPT / 4] : gg[1][k - PPT / 4];
+            if (P.td) {
+                // time-domain output (continuous FC, as rx_short_warp): element t + TT k of x
+                const fc_col d = P.td[m];
+                const long long base = (sy.sigma / N) * L + t;
+                const float2 phs = cscale(ph, sd.rx_s0 * rsqrtf((float)L));
+#pragma unroll
+                for (int k = 0; k < PPT; ++k)
+                    if (base + TT * k < d.len_out) orow[d.out_off + base + TT * k] = cmul(g0[0][k], phs);
+                team_bar<true>(bid, TT);  // next subband reuses the buffers
+                continue;
+            }
             team_bar<true>(bid, TT);
             team_fft<L, TT, PPT, -1, 1, true>(g0, b1, P.tw, N / L, t, true, bid, TT);
         } else {
@@ -740,11 +782,10 @@ FCW_DI void tx_short_all(const KParams& P, const Team& tm, const SymDev& sy, con
         if (2 * P.M <= tm.nwarp)
             tx_short_team<N, LU, teams_per_cta<N>()>(P, tm, sy, row, spec0, spec1, scr);
         else
-            tx_short_one<N, LU>(P, tm, sy, row, row_next, staged, spec0, spec1, scr, stw, 0, P.M);
+            tx_short_one<N, LU, false, 0, false>(P, tm, sy, row, row_next, staged, spec0, spec1, scr, stw, 0, P.M);
     } else if constexpr (LU > 0) {
         // uniform L: the next symbol's first subband is staged across calls
-        tx_short_one<N, LU, LU == 256, ZV, (LU > 32)>(P, tm, sy, row, row_next, staged, spec0, spec1, scr, stw, 0,
-                                                   P.M);
+        tx_short_one<N, LU, LU == 256, ZV, false>(P, tm, sy, row, row_next, staged, spec0, spec1, scr, stw, 0, P.M);
     } else {
         for (int g = 0; g < P.n_groups; ++g) {
             const int gs = P.grp_start[g], gc = P.grp_count[g];
@@ -1342,8 +1383,8 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) tx_kernel(const KP
             }
             if (!(P.dbg_skip & 1))
                 tx_short_all<N, LU, ZV>(P, tm, sy, in_u + (long long)n * P.row_len,
-                                    n + 1 < n1 ? in_u + (long long)(n + 1) * P.row_len : nullptr, n > nfirst,
-                                    spec0, spec1, S.scr, S.stw);
+                                        n + 1 < n1 && !P.td ? in_u + (long long)(n + 1) * P.row_len : nullptr,
+                                        n > nfirst && !P.td, spec0, spec1, S.scr, S.stw);
             team_sync<G>(g, TT);
             // bins no subband touches are zeroed in the same phase as the first
             // rank of secondary contributions (disjoint bins: one barrier less)

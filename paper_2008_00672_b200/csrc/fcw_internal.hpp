@@ -124,6 +124,8 @@ struct Plan {
     int Lmax = 0;
     bool zv = false;
     int n_zero_core = 0;  // zero-filled bins (the guard band of a zv plan excluded)
+    bool generic = false;  // run the generic (LU = 0) kernels even for a uniform L (continuous-FC TX plans
+                           // whose short paths carry the time-domain input only there, fcw_cont.cu)
     bool nb = false;      // narrowband: every subband span within 16 bins [nb_k0, nb_k0 + 16), N = 1024, L = 16
     int nb_k0 = 0;  // uniform L = 256, N = 4096, bins t + 16m (m in [5, 10]) inactive and windowed out
     // device tables (one allocation)
@@ -189,6 +191,7 @@ cudaError_t psd(const float2* wave, long long stride, long long len, int S, int 
 size_t rx_smem_bytes(const Plan& plan);
 void fill_common(const Plan& plan, KParams& kp);
 // fcw_capi.cpp: continuous FC with time-domain I/O (fcw_cont.cu)
+void plan_force_generic(fcw_plan* p);
 int tx_time_domain(const fcw_plan* p, const fc_col* td, const float2* streams, long long stream_stride,
                    float2* wave, long long wave_stride, int S, cudaStream_t st);
 int rx_time_domain(const fcw_plan* p, const fc_col* td, const float2* wave, long long wave_stride,

@@ -82,7 +82,7 @@ KernelPair pick(int N, int LU, bool zv = false, bool nb = false) {
 
 // The uniform short size the specialised kernels were built for, or 0.
 int uniform_L(const Plan& p) {
-    if (p.n_groups != 1 || p.N < 1024) return 0;
+    if (p.generic || p.n_groups != 1 || p.N < 1024) return 0;
     const int L = p.grp_L[0];
     return (L >= 16 && L <= 1024) ? L : 0;
 }
@@ -142,9 +142,18 @@ cudaError_t resident_per_sm(KernelFn k, size_t smem, int dev, int* per_sm) {
         *per_sm = it->second;
         return cudaSuccess;
     }
-    cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(k),
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
+    // The dynamic-SMEM attribute only ever grows: a plan with less SMEM must
+    // not lower it under a cached entry of a plan that needs more (which
+    // would then launch with "invalid argument").
+    static std::map<std::pair<const void*, int>, size_t> attr_max;
+    size_t& amax = attr_max[std::make_pair(reinterpret_cast<const void*>(k), dev)];
+    cudaError_t e = cudaSuccess;
+    if (smem > amax) {
+        e = cudaFuncSetAttribute(reinterpret_cast<const void*>(k), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
+        if (e != cudaSuccess) return e;
+        amax = smem;
+    }
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, reinterpret_cast<const void*>(k), kThreads, smem);
     if (e != cudaSuccess) return e;
     cache[key] = *per_sm;

@@ -22,6 +22,8 @@ CASES = [
     (2048, [512, 1024], [300, 1500], [1000, 2001]),
     (4096, [256] * 3, [3000, 3300, 3600], [2000, 2000, 1999]),
     (1024, [256, 256], [200, 700], [100, 257]),
+    (2048, [512], [1024], [3000]),  # uniform L >= 512: team-wide short transforms
+    (4096, [1024, 1024], [1000, 3000], [2500, 4100]),
 ]
 
 

@@ -171,6 +171,26 @@ def test_random_geometries(N, Ls, cps):
             assert rel_rms(out[u], want_p) <= TOL, (u, fused)
 
 
+def test_kernel_smem_attribute_across_plans():
+    """One generic kernel, plans with more / less / more dynamic SMEM: the
+    kernel's SMEM attribute must never be lowered under a larger plan (it was
+    once cached per (kernel, smem) and the smaller plan reset it)."""
+    rng = np.random.default_rng(7)
+    cps = [144] * 3
+    plans = []
+    for Ls in ([1024, 512], [512, 64], [1024, 512]):
+        subs, maps = _random_case(rng, 2048, Ls, cps)
+        plans.append((api.Plan(2048, cps, subs, maps), subs, maps))
+    for plan, subs, maps in plans:
+        grid = (rng.standard_normal((1, len(cps), plan.row_active))
+                + 1j * rng.standard_normal((1, len(cps), plan.row_active))).astype(np.complex64)
+        wave = plan.tx_host(grid, 1)
+        w = type("W", (), {})()
+        w.subbands, w.active_maps, w.B, w.N, w.cp = subs, maps, len(cps), 2048, cps
+        want, _ = oracle_tx(w, grid[0].astype(np.complex128))
+        assert rel_rms(wave[0], want) <= TOL
+
+
 @pytest.mark.parametrize("chunk", ["1", "3", "7", "280"])
 def test_chunk_boundaries_full_frame(chunk, monkeypatch):
     """Full 280-symbol C5 frame: every CTA-run boundary recomputes the carry of
