@@ -1381,10 +1381,13 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) tx_kernel(const KP
                 // FCW_TX_ACCUMULATE reads the waveform it adds to: bring the next symbol's span in too
                 if (P.accumulate) prefetch_l2(out_u + P.sym[n + 1].sigma, 8LL * (3 * N / 2));
             }
-            if (!(P.dbg_skip & 1))
+            if (!(P.dbg_skip & 1)) {
+                // time-domain input (continuous FC, ZV == 0 kernels only) stages within a symbol only
+                const bool cross = ZV != 0 || !P.td;
                 tx_short_all<N, LU, ZV>(P, tm, sy, in_u + (long long)n * P.row_len,
-                                        n + 1 < n1 && !P.td ? in_u + (long long)(n + 1) * P.row_len : nullptr,
-                                        n > nfirst && !P.td, spec0, spec1, S.scr, S.stw);
+                                        n + 1 < n1 && cross ? in_u + (long long)(n + 1) * P.row_len : nullptr,
+                                        n > nfirst && cross, spec0, spec1, S.scr, S.stw);
+            }
             team_sync<G>(g, TT);
             // bins no subband touches are zeroed in the same phase as the first
             // rank of secondary contributions (disjoint bins: one barrier less)
