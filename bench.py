@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--dry-run", action="store_true",
+                    help="control path only (no GPU): launch/rendezvous, sharding and the final gather on gloo")
     return ap.parse_args()
 
 
@@ -55,6 +57,28 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
+
+
+def self_launch_cmd(argv: list[str], n: int, port: int) -> list[str]:
+    """`bench.py --gpus N` (N > 1) outside torchrun relaunches itself under
+    torch.distributed.run, one rank per GPU (127.0.0.1 rendezvous)."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *argv]
+
+
+def maybe_self_launch(args) -> None:
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        import socket
+
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        r = subprocess.run(self_launch_cmd(sys.argv[1:], args.gpus, port))
+        sys.exit(r.returncode)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} (one rank per GPU)")
 
 
 def shard(total: int, rank: int, world: int) -> tuple[int, int]:
@@ -180,6 +204,26 @@ def cpu_reference(w, units: int, threads: int, fused: bool, steps: int = 1):
     return vals, kind, sample
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def product_library_loaded() -> bool:
+    """Whether this process has the product's CUDA library mapped."""
+    try:
+        with open("/proc/self/maps") as f:
+            return "libfcwave_b200" in f.read()
+    except Exception:
+        return False
+
+
 def cpu_threads() -> int:
     try:
         return len(os.sched_getaffinity(0))
@@ -188,6 +232,9 @@ def cpu_threads() -> int:
 
 
 def run_reference_arm(args, w):
+    """The reference's own CPU implementation of the path (oracle/_ref: the
+    unmodified fcwave sources + FFTW shim) on every host thread, on this arm's
+    workload geometry built from the oracle (no product code in this process)."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
@@ -202,9 +249,15 @@ def run_reference_arm(args, w):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": w.name, "units_sampled": units, "description": w.description},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
+        "config": {"workload": w.name, "units": w.units, "units_sampled": units,
+                   "sample_note": (f"each step times {units} of the workload's {w.units} units (one whole unit per "
+                                   "host thread); the metric is a rate, so the sample measures the same "
+                                   "Msamples/s the full workload would run at"),
+                   "rx_path": args.rx, "description": w.description},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "cpu_model": cpu_model(), "kind": kind,
+                         "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "product_library_loaded": product_library_loaded(),
     }
     print(json.dumps(line), flush=True)
 
@@ -315,16 +368,102 @@ class Runner:
         return (time.perf_counter() - t0) / n_steps
 
 
+def flops_per_unit(banks) -> dict:
+    """Nominal transform arithmetic of the algorithm as built, 5 n log2 n per
+    complex n-point transform (the usual FFT flop convention): per symbol TX
+    runs, per subband, the OFDM IDFT_L and the two block DFT_L (ofdm.cpp:97,
+    fc_core.cpp:76-90) and, once for all subbands, the two block IFFT_N; fused
+    RX runs the two block FFT_N once and, per subband, the IDFT_L / DFT_L pair
+    of Eq. (30) (fc_sync.cpp:195-243; direct RX: three L-transforms)."""
+    import math
+
+    def t(n):
+        return 5.0 * n * math.log2(n)
+
+    tx = rx_f = rx_d = 0.0
+    for b in banks:
+        sub = sum(t(s.L) for s in b.subbands)
+        tx += b.B * (3 * sub + 2 * t(b.N))
+        rx_f += b.B * (2 * sub + 2 * t(b.N))
+        rx_d += b.B * (3 * sub + 2 * t(b.N))
+    return {"tx": tx, "rx_fused": rx_f, "rx_direct": rx_d}
+
+
+def fp32_peak():
+    """Measured FP32 ceiling of this GPU type (tools/ubench_fp32.cu on the box,
+    committed as profiles/fp32_peak.json), else the nominal 148 SM x 128 lanes
+    x 2 flop x 1.965 GHz."""
+    p = os.path.join(ROOT, "profiles", "fp32_peak.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["ffma_tflops"]), "measured (profiles/fp32_peak.json, tools/ubench_fp32.cu FFMA)"
+    except Exception:
+        return 148 * 128 * 2 * 1.965e9 / 1e12, "nominal (148 SM x 128 FP32 lanes x 2 x 1.965 GHz)"
+
+
+def knobs() -> dict:
+    """FCW_* environment knobs in effect (none are set in a default run)."""
+    return {k: v for k, v in os.environ.items() if k.startswith("FCW_")}
+
+
+def dry_run(args, w) -> None:
+    """Control path without a GPU: rendezvous (gloo), sharding, the timing
+    max-reduce and the final gather, exactly as the GPU arm runs them."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world, _ = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+    u0, S = shard(w.units, rank, world)
+    t = torch.tensor([float(rank + 1)], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    g = gather_stats(dist if world > 1 else None, torch.tensor([float(u0), float(S), 0.0, 0.0, 0.0, 0.0],
+                                                            dtype=torch.float64), world)
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "units": w.units, "max_t": float(t.item()),
+                          "shards": [[int(r[0]), int(r[1])] for r in g]}), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def gather_stats(dist, row, world):
+    """Final gather (outside the timed region): every rank's per-shard row."""
+    import torch
+
+    if dist is None:
+        return [row.tolist()]
+    rows = [torch.zeros_like(row) for _ in range(world)]
+    dist.all_gather(rows, row)
+    return [r.tolist() for r in rows]
+
+
 def main():
     args = parse()
+    maybe_self_launch(args)
     from paper_2008_00672_b200 import configs
 
+    if args.impl == "reference":
+        import oracle as O
+
+        # the reference arm builds its geometry from the oracle: no product code loads here
+        w = configs.get(args.config, geom=O.Geometry())
+        if args.units:
+            w.units = args.units
+        run_reference_arm(args, w)
+        return
+    if args.dry_run:
+        w = configs.get(args.config, geom=__import__("oracle").Geometry())
+        if args.units:
+            w.units = args.units
+        dry_run(args, w)
+        return
     w = configs.get(args.config)
     if args.units:
         w.units = args.units
-    if args.impl == "reference":
-        run_reference_arm(args, w)
-        return
 
     import torch
 
@@ -384,12 +523,29 @@ def main():
     total_samples = w.units * frame_samples(w)
     value = total_samples / (ms_per_step * 1e-3) / 1e6
 
+    # final gather (north_star), outside the timed region: per-shard link
+    # statistics of the last step's RX output against the seeded transmit bits
+    ls_num = ls_den = 0.0
+    ls_err = ls_bits = 0
+    for i, (b, p) in enumerate(zip(run.banks, run.plans)):
+        st = p.link_stats(run.outs[i], S, SEED + i, u0, w.bits_per_symbol, stream=stream)
+        ls_num += float(st.evm_num.sum())
+        ls_den += float(st.evm_den.sum())
+        ls_err += int(st.bit_errors.sum())
+        ls_bits += int(st.n_bits.sum())
+    rows = gather_stats(dist, torch.tensor([float(u0), float(S), ls_num, ls_den, float(ls_err), float(ls_bits)],
+                                           dtype=torch.float64, device=dev), world)
+
     # roofline of the dominant kernel (algorithmic bytes per launch / mean launch time)
     ab = run.algorithmic_bytes_per_unit()
     peak, peak_src = hbm_peak()
     dom = "rx" if rx_avg > tx_avg else "tx"
     dom_ms = max(rx_avg, tx_avg)
     achieved = ab[dom] * S / (dom_ms * 1e-3) / 1e9
+    fl = flops_per_unit(run.banks)
+    dom_fl = fl["tx"] if dom == "tx" else fl["rx_fused" if fused else "rx_direct"]
+    f_ach = dom_fl * S / (dom_ms * 1e-3) / 1e12
+    f_peak, f_src = fp32_peak()
     traffic = None
     prof = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(prof):
@@ -421,19 +577,26 @@ def main():
                "d2h_bytes_per_step": wave_b + grid_b, "steps": max(1, args.e2e_steps),
                "path": ("fcw_tx_host + fcw_rx_host (pinned host buffers, 2-stream H2D/kernel/D2H pipeline per "
                         "call); duplex: TX of step k on one host thread overlaps RX of step k-1's waveform on "
-                        "another (two plans), so both PCIe directions carry traffic"
+                        "another (two plans), so both PCIe directions carry traffic; serial_value: TX then RX"
                         if not run.mixed else "pinned H2D + MixedNumerology.tx/rx + D2H"),
-               "serial_value": total_samples / serial_s / 1e6}
+               "serial_value": total_samples / serial_s / 1e6,
+               "bound": "PCIe: every step moves the grid and the waveform both ways (profiles/r01/pcie_bw.txt)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = cpu_threads()
         units = max(1, min(threads, w.units))
         vals, kind, sample = cpu_reference(w, units, threads, fused, steps=1)
-        cpu = {"value": vals[0], "unit": UNIT, "cores": threads, "kind": kind, "sample": sample}
+        cpu = {"value": vals[0], "unit": UNIT, "cores": threads, "cpu_model": cpu_model(), "kind": kind,
+               "sample": sample}
 
     if rank == 0:
+        from paper_2008_00672_b200.api import evm_db_from_sums
+
         N = max(b.N for b in run.banks)
+        hbm_frac, fp_frac = achieved / peak, f_ach / f_peak
+        g_num, g_den = sum(r[2] for r in rows), sum(r[3] for r in rows)
+        g_err, g_bits = int(sum(r[4] for r in rows)), int(sum(r[5] for r in rows))
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
@@ -443,16 +606,28 @@ def main():
                        "N": [b.N for b in run.banks], "rx_path": args.rx,
                        "l2": "inputs larger than L2 (working set %.1f GB)" % (ab["total"] * w.units / 2 / 1e9)
                        if ab["total"] * w.units / 2 > 126e6 else "working set fits L2 (small config)",
-                       "description": w.description},
-            "roofline": {"bound": "hbm", "kernel": f"{dom}_kernel<{N}>", "achieved": achieved, "peak": peak,
-                         "unit": "GB/s", "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                       "description": w.description, "knobs": knobs()},
+            "roofline": {"bound": "hbm" if hbm_frac >= fp_frac else "fp32",
+                         "kernel": f"{dom}_kernel<{N}>", "achieved": achieved, "peak": peak,
+                         "unit": "GB/s", "frac": hbm_frac, "traffic": traffic, "peak_source": peak_src,
                          "algorithmic_bytes_per_unit": ab[dom],
-                         "txrx_achieved_gbs": both_gbs, "txrx_frac": both_gbs / peak},
+                         "txrx_achieved_gbs": both_gbs, "txrx_frac": both_gbs / peak,
+                         "fp32": {"achieved": f_ach, "peak": f_peak, "unit": "TFLOP/s", "frac": fp_frac,
+                                  "peak_source": f_src, "algorithmic_flops_per_unit": dom_fl,
+                                  "model": "5 n log2 n per complex transform (bench.flops_per_unit)",
+                                  "ncu": "profiles/r02/SUMMARY.md (IPC, FMA-pipe %)"},
+                         "note": ("achieved/peak/frac are the HBM roofline north_star names; bound says which "
+                                  "of HBM and FP32 the kernel is closer to")},
             "kernels_ms": {"tx": tx_avg, "rx": rx_avg},
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks,
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "gather": {"ranks": world, "units": int(sum(r[1] for r in rows)),
+                       "shards": [[int(r[0]), int(r[1])] for r in rows],
+                       "evm_db": evm_db_from_sums(g_num, g_den) if g_den > 0 else None,
+                       "bit_errors": g_err, "n_bits": g_bits,
+                       "what": "last step's RX grids vs the seeded transmit bits (fcw_link_stats), per shard"},
         }
         print(json.dumps(line), flush=True)
     if dist:

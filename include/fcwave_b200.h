@@ -179,6 +179,12 @@ int fcw_apply_channel(const void* wave_in, void* wave_out, int64_t wave_unit_str
 int fcw_wave_power(const fcw_plan* plan, const void* wave, int64_t wave_unit_stride, int64_t wave_len, int S,
                    int64_t begin, int64_t end, double* power, void* stream);
 
+/* Zero samples [begin, end) of S device waveforms (stream-ordered 2-D
+ * memset).  MixedNumerology composition: the spans the first bank does not
+ * write before later banks accumulate onto them (there is no reference
+ * counterpart; the reference allocates zeroed vectors, fc_sync.cpp:103,133). */
+int fcw_wave_zero(void* wave, int64_t wave_unit_stride, int S, int64_t begin, int64_t end, void* stream);
+
 /* Welch PSD (metrics.cpp:128-155, row f4) of S device waveforms of wave_len
  * samples: Hann windows of seg_len (a power of two in [64, 4096]) hopping
  * lround(seg_len (1 - overlap_frac)), |FFT|^2 averaged and scaled by

@@ -75,6 +75,10 @@ def lib():
         L.fco_combined_length.argtypes = [C.c_int, _i32p, C.POINTER(FcoParams)]
         L.fco_combined_length.restype = C.c_int64
         L.fco_design_window.argtypes = [C.c_int, C.c_int, C.c_int, _f64p]
+        L.fco_bin_map.argtypes = [C.c_int, C.c_int, C.c_int, _i32p, _i32p]
+        L.fco_bin_map.restype = None
+        L.fco_rx_start.argtypes = [C.c_int64, C.c_int, C.c_int, _i32p, C.c_int]
+        L.fco_rx_start.restype = C.c_int64
         L.fco_centered_active_map.argtypes = [C.c_int, C.c_int, C.c_int, _i32p]
         for f in (L.fco_block_phase,):
             f.argtypes = [C.c_int64, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]
@@ -230,6 +234,47 @@ def cp_schedule(scs_khz: int, n_fft: int, n_symbols: int) -> list[int]:
     return out.tolist()
 
 
+def nr_cp_schedule(scs_khz: int, n_fft: int, n_symbols: int) -> list[int]:
+    """5G-NR normal CP (3GPP TS 38.211 §5.3.1), restated independently of the
+    product's fcw_nr_cp_schedule: N_CP = 144 kappa 2^-mu Tc, plus 16 kappa Tc on
+    the first symbol of every 0.5 ms (l mod 7 * 2^mu == 0).  In samples at
+    fs = n_fft * scs: 144 n_fft / 2048 and 16 * 2^mu * n_fft / 2048 (30 kHz,
+    N = 4096: 288 / 352).  Same validation shape as the reference's
+    cp_schedule (numerology.cpp:17-42)."""
+    if n_fft < 16 or n_fft & (n_fft - 1):
+        raise ValueError("n_fft must be a power of two >= 16")
+    mu2 = scs_khz // 15
+    if scs_khz <= 0 or scs_khz % 15 or mu2 & (mu2 - 1):
+        raise ValueError("scs_khz must be 15*2^k")
+    if n_symbols < 1:
+        raise ValueError("n_symbols must be >= 1")
+    if (144 * n_fft) % 2048 or (16 * mu2 * n_fft) % 2048:
+        raise ValueError("n_fft does not scale the CP pattern to integers")
+    short = 144 * n_fft // 2048
+    extra = 16 * mu2 * n_fft // 2048
+    return [short + (extra if n % (7 * mu2) == 0 else 0) for n in range(n_symbols)]
+
+
+class Geometry:
+    """Workload geometry backend for paper_2008_00672_b200.configs built from
+    this oracle only (bench.py's reference arm: no product library loaded)."""
+
+    design_window = staticmethod(lambda L, n, tb: design_window(L, n, tb))
+    centered_active_map = staticmethod(lambda L, n, skip_dc=True: centered_active_map(L, n, skip_dc))
+    cp = staticmethod(lambda scs, N, B: cp_schedule(scs, N, B))
+    nr_cp = staticmethod(lambda scs, N, B: nr_cp_schedule(scs, N, B))
+
+    @staticmethod
+    def subband(**kw):
+        from types import SimpleNamespace
+
+        kw.setdefault("n_active", 0)
+        kw.setdefault("n_tb", 0)
+        kw.setdefault("l_ofdm", kw["L"])
+        kw["window"] = np.ascontiguousarray(np.asarray(kw["window"], np.float64))
+        return SimpleNamespace(**kw)
+
+
 def cp_truncate(n_cp: int, I: int) -> tuple[int, int]:
     a, b = C.c_int(), C.c_int()
     lib().fco_cp_truncate(n_cp, I, C.byref(a), C.byref(b))
@@ -243,6 +288,21 @@ def symbol_sigma(n: int, cp, N: int) -> int:
 def combined_length(B: int, cp, p: Params) -> int:
     pc = p.c()
     return int(lib().fco_combined_length(B, _i32(cp), C.byref(pc)))
+
+
+def bin_map(L: int, c: int, N: int) -> tuple[np.ndarray, np.ndarray]:
+    """(q, b) per shifted index p0 (fc_core.cpp:80-84): the map the oracle's
+    synth / analysis use."""
+    q, b = np.zeros(L, np.int32), np.zeros(L, np.int32)
+    lib().fco_bin_map(L, c, N, q, b)
+    return q, b
+
+
+def rx_starts(useful0: int, cp, N: int, L: int) -> np.ndarray:
+    """rx_segment window starts useful0 - N_L + sigma_n (fc_sync.cpp:148)."""
+    p = derive_params(N, L)
+    cpa = _i32(cp)
+    return np.array([lib().fco_rx_start(useful0, p.N_L, n, cpa, N) for n in range(len(cp))], np.int64)
 
 
 def design_window(L: int, n_pass: int, n_tb: int) -> np.ndarray:

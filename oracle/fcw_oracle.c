@@ -183,6 +183,23 @@ void fco_fft(double* d, int n, int inverse) {
 
 static double* zalloc(size_t ncomplex) { return (double*)calloc(ncomplex * 2 + 2, sizeof(double)); }
 
+/* The subband bin map of synth_core / rx_block_freq (fc_core.cpp:80-84,
+ * fc_sync.cpp:183-187): shifted index p0 in [0, L) sits on long-transform bin
+ * q = (c - ceil(L/2) + p0) mod N and carries short-transform bin
+ * b = (p0 + L/2) mod L. */
+void fco_bin_map(int L, int c, int N, int* q, int* b) {
+    const int half = (L + 1) / 2;
+    for (int p0 = 0; p0 < L; ++p0) {
+        b[p0] = (p0 + L / 2) % L;
+        q[p0] = (int)mod64((int64_t)c - half + p0, N);
+    }
+}
+
+/* rx_segment's window start (fc_sync.cpp:148): useful0 - N_L + sigma_n */
+int64_t fco_rx_start(int64_t useful0, int N_L, int n, const int* cp, int N) {
+    return useful0 - N_L + fco_symbol_sigma(n, cp, N);
+}
+
 /* fc_core.cpp:76-90 synth_core after the OLA analysis window
  * (sfb_block_ola, fc_core.cpp:115-124).  out: N complex. */
 static void synth_block(const double* xw, int L, int c, const double* window, int N, double pr,
@@ -191,15 +208,16 @@ static void synth_block(const double* xw, int L, int c, const double* window, in
     memcpy(X, xw, sizeof(double) * 2 * (size_t)L);
     fco_fft(X, L, 0);
     memset(out, 0, sizeof(double) * 2 * (size_t)N);
-    const int half = (L + 1) / 2;
+    int* qm = (int*)malloc(sizeof(int) * 2 * (size_t)L);
+    fco_bin_map(L, c, N, qm, qm + L);
     for (int p0 = 0; p0 < L; ++p0) {
-        const int b = (p0 + L / 2) % L;
-        const int q = (int)mod64((int64_t)c - half + p0, N);
+        const int b = qm[L + p0], q = qm[p0];
         const double wr = window[p0] * X[2 * b], wi = window[p0] * X[2 * b + 1];
         out[2 * q] = pr * wr - pi * wi;
         out[2 * q + 1] = pr * wi + pi * wr;
     }
     fco_fft(out, N, 1);
+    free(qm);
     free(X);
 }
 
@@ -315,15 +333,16 @@ int fco_rx_block_freq(const double* y, int L, int c, const double* window, const
     double* Y = zalloc((size_t)N);
     memcpy(Y, y, sizeof(double) * 2 * (size_t)N);
     fco_fft(Y, N, 0);
-    const int half = (L + 1) / 2;
+    int* qm = (int*)malloc(sizeof(int) * 2 * (size_t)L);
+    fco_bin_map(L, c, N, qm, qm + L);
     for (int p0 = 0; p0 < L; ++p0) {
-        const int b = (p0 + L / 2) % L;
-        const int q = (int)mod64((int64_t)c - half + p0, N);
+        const int b = qm[L + p0], q = qm[p0];
         const double vr = window[p0] * Y[2 * q], vi = window[p0] * Y[2 * q + 1];
         /* conj(phase) * v */
         g[2 * b] = ph_re * vr + ph_im * vi;
         g[2 * b + 1] = ph_re * vi - ph_im * vr;
     }
+    free(qm);
     free(Y);
     return 0;
 }
@@ -416,7 +435,7 @@ int fco_rx_discontinuous(const double* wave, int64_t len, int64_t useful0, int N
     double* g1 = zalloc((size_t)L);
     int rc = 0;
     for (int n = 0; n < B; ++n) {
-        const int64_t start = useful0 - p.N_L + fco_symbol_sigma(n, cp, N);
+        const int64_t start = fco_rx_start(useful0, p.N_L, n, cp, N);
         if (start < 0 || start + 3 * N / 2 > len) {
             rc = 1;
             break;

@@ -39,6 +39,8 @@ int fco_cp_schedule(int scs_khz, int n_fft, int n_symbols, int* out);
 void fco_cp_truncate(int n_cp_high, int I, int* l_cp, int* extrap);
 int64_t fco_cp_partial_sum(const int* cp, int n);
 int64_t fco_symbol_sigma(int n, const int* cp, int N);
+void fco_bin_map(int L, int c, int N, int* q, int* b);
+int64_t fco_rx_start(int64_t useful0, int N_L, int n, const int* cp, int N);
 int64_t fco_combined_length(int B, const int* cp, const fco_params* p);
 int fco_design_window(int L, int n_pass, int n_tb, double* w);
 int fco_centered_active_map(int l_ofdm, int n_active, int skip_dc, int* bins);

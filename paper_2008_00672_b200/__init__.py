@@ -5,29 +5,25 @@ The compute path is hand-written sm_100a CUDA in ``csrc/`` behind the C ABI
 ``include/fcwave_b200.h``; this package is the Python host mirror of the
 reference's operator API.  There is no CPU fallback.
 """
-from .api import (  # noqa: F401
-    CpSchedule,
-    FcParams,
-    Numerology,
-    PinnedBuffer,
-    Plan,
-    QamGrid,
-    SubbandConfig,
-    Waveform,
-    centered_active_map,
-    combined_length,
-    cp_schedule,
-    cp_truncate,
-    derive_fc_params,
-    design_window,
-    first_block_overlap,
-    make_numerology,
-    nr_cp_schedule,
-    rx_discontinuous,
-    rx_discontinuous_all,
-    symbol_sigma,
-    tx_discontinuous,
+# The host API loads the CUDA library on first use; submodules that need no
+# product code (``configs`` with an outside geometry backend) import without it.
+_API = (
+    "CpSchedule", "FcParams", "Numerology", "PinnedBuffer", "Plan", "QamGrid", "SubbandConfig", "Waveform",
+    "centered_active_map", "combined_length", "cp_schedule", "cp_truncate", "derive_fc_params", "design_window",
+    "first_block_overlap", "make_numerology", "nr_cp_schedule", "rx_discontinuous", "rx_discontinuous_all",
+    "symbol_sigma", "tx_discontinuous",
 )
-from ._lib import FcwError  # noqa: F401
-
+__all__ = list(_API) + ["FcwError"]
 __version__ = "0.1.0"
+
+
+def __getattr__(name):
+    if name in _API:
+        from . import api
+
+        return getattr(api, name)
+    if name == "FcwError":
+        from ._lib import FcwError
+
+        return FcwError
+    raise AttributeError(name)

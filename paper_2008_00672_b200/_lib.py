@@ -29,7 +29,7 @@ EXPORTS = [
     "fcw_centered_active_map", "fcw_symbol_sigma", "fcw_combined_length", "fcw_last_error", "fcw_version",
     "fcw_link_stats", "fcw_awgn", "fcw_wave_power", "fcw_psd", "fcw_draw_tdl", "fcw_apply_channel",
     "fcw_cont_plan_create", "fcw_cont_plan_destroy", "fcw_cont_plan_get_info", "fcw_tx_continuous",
-    "fcw_rx_continuous",
+    "fcw_rx_continuous", "fcw_wave_zero",
 ]
 
 
@@ -107,6 +107,7 @@ def lib() -> C.CDLL:
     L.fcw_wave_power.argtypes = [vp, vp, i64, i64, C.c_int, i64, i64, C.POINTER(C.c_double), vp]
     L.fcw_draw_tdl.argtypes = [vp, vp, C.c_int, C.c_double, C.c_uint64, vp, vp]
     L.fcw_apply_channel.argtypes = [vp, vp, i64, i64, C.c_int, vp, vp, C.c_int, vp]
+    L.fcw_wave_zero.argtypes = [vp, i64, C.c_int, i64, i64, vp]
     L.fcw_psd.argtypes = [vp, i64, i64, C.c_int, C.c_int, C.c_double, C.POINTER(C.c_double), vp]
     L.fcw_cont_plan_create.argtypes = [C.POINTER(vp), C.c_int, C.c_double, vp, C.c_int, C.POINTER(C.c_int64), i64,
                                        C.c_int]

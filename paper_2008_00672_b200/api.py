@@ -102,13 +102,12 @@ def _i32p(a: np.ndarray):
 
 
 def make_numerology(scs_khz: int, n_fft: int) -> Numerology:
-    """numerology.cpp:17-27 (validation via the C ABI)."""
-    tmp = np.zeros(1, np.int32)
+    """numerology.cpp:17-27: same checks and messages, in the host layer (the
+    C ABI validates again in every call that takes a numerology)."""
     if n_fft < 16 or n_fft & (n_fft - 1):
         raise ValueError("n_fft must be a power of two >= 16")
     if scs_khz <= 0 or scs_khz % 15 or (scs_khz // 15) & (scs_khz // 15 - 1):
         raise ValueError("scs_khz must be 15*2^k")
-    del tmp
     return Numerology(scs_khz, n_fft, 7)
 
 
@@ -369,8 +368,12 @@ class MixedNumerology:
         self.frame_samples = max(p.frame_samples for p, _ in self.banks)
 
     def tx(self, grids, wave, S: int, stream=None) -> None:
-        """grids[i]: device packed grid of bank i; wave: device complex64 [S][Q]."""
+        """grids[i]: device packed grid of bank i; wave: device complex64 [S][Q].
+        Samples outside bank 0's span are zeroed first: later banks add onto them."""
         base = _dev_ptr(wave)
+        p0, off0 = self.banks[0]
+        check(lib().fcw_wave_zero(base, self.Q, S, 0, off0, _stream_ptr(stream)))
+        check(lib().fcw_wave_zero(base, self.Q, S, off0 + p0.Q, self.Q, _stream_ptr(stream)))
         for i, ((p, off), g) in enumerate(zip(self.banks, grids)):
             p.tx(g, base + 8 * off, S, stream=stream, wave_stride=self.Q, accumulate=i > 0)
 

@@ -89,7 +89,7 @@ void pick_schedule(const fcw::Plan& p, int S, bool tx, fcw::KParams& kp) {
             }
         }
     const int G = (p.N >= 512 && p.N <= 4096) ? 4096 / p.N : 1;
-    const long long teams = 2LL * 148 * G;
+    const long long teams = 2LL * fcw::device_sms() * G;  // 2 resident CTAs per SM
     const long long per_team = (long long)p.B * std::max(S, 1) / teams;
     const char* sched = std::getenv("FCW_SCHED");  // dev A/B knob: "static" keeps balanced static ranges
     const bool force_static = sched && std::strcmp(sched, "static") == 0;
@@ -112,7 +112,18 @@ int set_cuda_error(cudaError_t e, const char* where) { return cuda_fail(e, where
 struct fcw_plan : fcw::Plan {};
 
 namespace fcw {
-void plan_force_generic(fcw_plan* p) { p->generic = true; }
+// Generic (mixed-L) kernels: the zero-bin (zv) and narrowband (nb) kernel
+// variants and their trimmed zero lists no longer apply.
+void plan_force_generic(fcw_plan* p) {
+    p->generic = true;
+    plan_clear_special(p);
+}
+// Drop the zv / nb specialisations (their kernels carry no time-domain I/O):
+// the plan then runs the plain uniform-L kernels with the full zero list.
+void plan_clear_special(fcw_plan* p) {
+    p->zv = false;
+    p->nb = false;
+}
 
 // Continuous FC with time-domain I/O (fcw_cont.cu): the fused kernels read
 // the subband streams (TX) or write the output streams (RX) through the
@@ -797,6 +808,19 @@ int fcw_wave_power(const fcw_plan* p, const void* wave, int64_t wave_stride, int
     const cudaError_t e = fcw::wave_power(static_cast<const float2*>(wave), wave_stride, S, begin, end, power,
                                           static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "wave_power");
+    return FCW_OK;
+}
+
+int fcw_wave_zero(void* wave, int64_t wave_stride, int S, int64_t begin, int64_t end, void* stream) {
+    if (!wave && S > 0) return fail(FCW_EINVAL, "null argument");
+    if (S < 0 || begin < 0 || end < begin || (S > 1 && wave_stride < end))
+        return fail(FCW_EINVAL, "invalid zero span");
+    if (S == 0 || end == begin) return FCW_OK;
+    const size_t pitch = sizeof(float2) * (size_t)(S > 1 ? wave_stride : end);
+    const cudaError_t e = cudaMemset2DAsync(static_cast<float2*>(wave) + begin, pitch, 0,
+                                            sizeof(float2) * (size_t)(end - begin), (size_t)S,
+                                            static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "wave_zero");
     return FCW_OK;
 }
 

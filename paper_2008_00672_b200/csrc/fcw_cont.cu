@@ -301,6 +301,10 @@ int fcw_cont_plan_create(fcw_cont_plan** out, int N, double overlap, const fcw_s
         // the TX thread (L <= 32) and warp (L >= 512) paths carry the
         // time-domain input in the generic kernels only (tx_short_one)
         if (p->td_tx && (big || (uni && sbs[0].L <= 32))) fcw::plan_force_generic(p->tx);
+        // the zv / nb kernel variants carry no time-domain I/O (nor the
+        // bounded window load that replaces rx_continuous's zero padding)
+        if (p->td_tx) fcw::plan_clear_special(p->tx);
+        if (p->td_rx) fcw::plan_clear_special(p->rx);
     }
     int off = 0;
     for (int m = 0; m < M; ++m) {

@@ -31,6 +31,14 @@ namespace fcw {
 
 constexpr int kPPT = 16;  // long-transform points per thread and block
 
+// Dev-only stage-timing knob (FCW_DEBUG_SKIP, bit 1: short stage, bit 2: long
+// transform).  Compiled out of the release library (FCW_DEV_KNOBS=0): the
+// product kernels always run every stage.
+#ifndef FCW_DEV_KNOBS
+#define FCW_DEV_KNOBS 0
+#endif
+#define FCW_SKIP(P, bit) (FCW_DEV_KNOBS && ((P).dbg_skip & (bit)))
+
 // Bin-class entry (plan, per class and DFT bin b), 8 bytes:
 //   x = (inv[b] & 0xffff) | sec(p0) << 16, y = bits(w[p0]), p0 = b ^ L/2;
 //   sec = -2: zero weight (no contribution), -1: primary (spectrum slot q),
@@ -1381,7 +1389,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) tx_kernel(const KP
                 // FCW_TX_ACCUMULATE reads the waveform it adds to: bring the next symbol's span in too
                 if (P.accumulate) prefetch_l2(out_u + P.sym[n + 1].sigma, 8LL * (3 * N / 2));
             }
-            if (!(P.dbg_skip & 1)) {
+            if (!FCW_SKIP(P, 1)) {
                 // time-domain input (continuous FC, ZV == 0 kernels only) stages within a symbol only
                 const bool cross = ZV != 0 || !P.td;
                 tx_short_all<N, LU, ZV>(P, tm, sy, in_u + (long long)n * P.row_len,
@@ -1432,13 +1440,13 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) tx_kernel(const KP
                     }
                 }
                 float2* const bufs[2] = {spec0, spec1};
-                if (!(P.dbg_skip & 2))
+                if (!FCW_SKIP(P, 2))
                     team_fft<N, T, kPPT, +1, 2, true, long_twl<N>(), ZG>(v, bufs, long_twl<N>() ? S.ltw : P.tw, 1,
                                                                         gtid, act, G == 1 ? 0 : 1 + g, TT);
             }
             // every thread has read its carry before it is overwritten: the long
             // transform's exchange barriers already order that for N >= 512
-            if (N < 512 || (P.dbg_skip & 2)) team_sync<G>(g, TT);
+            if (N < 512 || FCW_SKIP(P, 2)) team_sync<G>(g, TT);
             // symbol-wise overlap-add: block 0 at 0, block 1 at N/2, carry from n-1
             if (act) {
                 const bool emit = n >= n0;
@@ -1530,7 +1538,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) rx_kernel(const KP
             } else {
             {
                 float2* const bufs[2] = {spec0, spec1};
-                if (!(P.dbg_skip & 2))
+                if (!FCW_SKIP(P, 2))
                     team_fft<N, T, kPPT, -1, 2, true, long_twl<N>()>(v, bufs, long_twl<N>() ? S.ltw : P.tw, 1, gtid, act,
                                                                     G == 1 ? 0 : 1 + g, TT);
             }
@@ -1551,7 +1559,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) rx_kernel(const KP
             }
             }
             team_sync<G>(g, TT);
-            if (!(P.dbg_skip & 1))
+            if (!FCW_SKIP(P, 1))
                 rx_short_all<N, LU, ZV>(P, tm, sy, spec0, spec1, out_u + (long long)n * P.row_len, S.scr, S.stw);
         }
     }

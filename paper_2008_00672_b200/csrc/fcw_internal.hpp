@@ -163,6 +163,9 @@ int set_cuda_error(cudaError_t e, const char* where);
 // per-device stream-ordered scratch pool that keeps its memory (no OS
 // re-allocation after every synchronisation)
 cudaError_t scratch_pool(int dev, cudaMemPool_t* out);
+// SM count of the current device (queried once per device; grid sizing and
+// the work schedule use it instead of a hard-coded 148).
+int device_sms();
 template <class T>
 cudaError_t scratch_alloc(T** p, size_t bytes, cudaStream_t st) {
     int dev = 0;
@@ -192,6 +195,7 @@ size_t rx_smem_bytes(const Plan& plan);
 void fill_common(const Plan& plan, KParams& kp);
 // fcw_capi.cpp: continuous FC with time-domain I/O (fcw_cont.cu)
 void plan_force_generic(fcw_plan* p);
+void plan_clear_special(fcw_plan* p);
 int tx_time_domain(const fcw_plan* p, const fc_col* td, const float2* streams, long long stream_stride,
                    float2* wave, long long wave_stride, int S, cudaStream_t st);
 int rx_time_domain(const fcw_plan* p, const fc_col* td, const float2* wave, long long wave_stride,

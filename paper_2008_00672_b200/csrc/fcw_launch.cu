@@ -220,6 +220,20 @@ cudaError_t scratch_pool(int dev, cudaMemPool_t* out) {
     return cudaSuccess;
 }
 
+int device_sms() {
+    static std::mutex mu;
+    static std::map<int, int> sms;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = sms.find(dev);
+    if (it != sms.end()) return it->second;
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) return 148;
+    sms[dev] = n;
+    return n;
+}
+
 void fill_common(const Plan& p, KParams& kp) {
     kp.N = p.N;
     kp.B = p.B;
@@ -251,8 +265,12 @@ void fill_common(const Plan& p, KParams& kp) {
     kp.stab_len = stab_len(p);
     kp.tw16_len = tw16_len(p);
     kp.stage_off = p.Lmax >= 64 ? scratch_one(p) : 0;
+#if FCW_DEV_KNOBS
     const char* dbg = std::getenv("FCW_DEBUG_SKIP");
     kp.dbg_skip = dbg ? std::atoi(dbg) : 0;
+#else
+    kp.dbg_skip = 0;
+#endif
 }
 
 size_t tx_smem_bytes(const Plan& p) { return smem_bytes(p, true, false); }
@@ -321,7 +339,8 @@ cudaError_t launch_gen_qam(const Plan& p, uint64_t seed, long long unit0, int S,
     const long long per_unit = (long long)p.B * p.row_active;
     const long long total = per_unit * S;
     int grid = (int)((total + 255) / 256);
-    if (grid > 148 * 64) grid = 148 * 64;
+    const int cap = device_sms() * 64;
+    if (grid > cap) grid = cap;
     if (grid < 1) grid = 1;
     gen_qam_kernel<<<grid, 256, 0, st>>>(seed, unit0, S, per_unit, bits, out);
     return cudaGetLastError();

@@ -327,7 +327,7 @@ cudaError_t link_stats(const Plan& p, const float2* grid, long long stride, int 
 cudaError_t awgn(float2* wave, long long stride, long long len, int S, double sigma2, uint64_t seed,
                  long long unit0, cudaStream_t st) {
     const long long total = (long long)S * len;
-    int grid = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
+    int grid = (int)std::min<long long>((total + 255) / 256, (long long)device_sms() * 16);
     if (grid < 1) grid = 1;
     awgn_kernel<<<grid, 256, 0, st>>>(wave, stride, len, S, sqrt(sigma2), seed, unit0);
     return cudaGetLastError();
@@ -412,10 +412,13 @@ cudaError_t psd(const float2* wave, long long stride, long long len, int S, int 
 
 cudaError_t apply_channel(const float2* in, float2* out, long long stride, long long len, int S, const int* delays,
                           const float2* gains, int n_taps, cudaStream_t st) {
-    int* d = nullptr;
-    cudaError_t e = scratch_alloc(&d, (sizeof(int) + sizeof(float2)) * (size_t)S * n_taps, st);
+    // gains first: the float2 block must stay 8-byte aligned whatever S * n_taps is
+    const size_t gbytes = sizeof(float2) * (size_t)S * n_taps;
+    void* blk = nullptr;
+    cudaError_t e = scratch_alloc(&blk, gbytes + sizeof(int) * (size_t)S * n_taps, st);
     if (e != cudaSuccess) return e;
-    float2* g = reinterpret_cast<float2*>(d + (size_t)S * n_taps);
+    float2* g = static_cast<float2*>(blk);
+    int* d = reinterpret_cast<int*>(static_cast<char*>(blk) + gbytes);
     e = cudaMemcpyAsync(d, delays, sizeof(int) * (size_t)S * n_taps, cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess) e = cudaMemcpyAsync(g, gains, sizeof(float2) * (size_t)S * n_taps, cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess) {
@@ -423,7 +426,7 @@ cudaError_t apply_channel(const float2* in, float2* out, long long stride, long 
         channel_kernel<<<dim3(gx, S), 256, 0, st>>>(in, out, stride, len, d, g, n_taps);
         e = cudaGetLastError();
     }
-    const cudaError_t f = cudaFreeAsync(d, st);
+    const cudaError_t f = cudaFreeAsync(blk, st);
     if (e == cudaSuccess) e = f;
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // host tap arrays may be released on return
     return e;

@@ -41,6 +41,35 @@ def case(name, N, Ls, cs, windows, cp, rng, qam_bits=None):
     print(name, len(wave))
 
 
+def case_workload(name, w, B, seed):
+    """A BASELINE workload's exact geometry (paper_2008_00672_b200.configs with
+    the oracle's geometry backend) over its first B symbols, seeded 2^bits-QAM
+    on the active bins.  Compact format: the packed grid and all outputs are
+    stored as complex64 (the grid is rounded to fp32 BEFORE the reference runs,
+    so the reference and the GPU consume identical inputs); outputs are the
+    reference's full L-bin RX columns of every subband, concatenated."""
+    cp = w.cp[:B]
+    A = sum(len(m) for m in w.active_maps)
+    packed = O.gen_grid(seed, 0, 1, B, A, w.bits_per_symbol)[0].astype(np.complex64)
+    grids, off = [], 0
+    for s, bins in zip(w.subbands, w.active_maps):
+        g = np.zeros((B, s.L), complex)
+        g[:, bins] = packed[:, off:off + len(bins)]
+        grids.append(g)
+        off += len(bins)
+    Ls, cs, wins = [s.L for s in w.subbands], [s.c for s in w.subbands], [s.window for s in w.subbands]
+    wave, u0 = O.Ref.tx_discontinuous(grids, Ls, cs, wins, cp, w.N)
+    out = dict(N=w.N, cp=np.array(cp), Ls=np.array(Ls), cs=np.array(cs), windows=np.concatenate(wins),
+               active=np.concatenate([np.asarray(m, np.int32) for m in w.active_maps]),
+               n_active=np.array([len(m) for m in w.active_maps]), packed=packed,
+               wave=wave.astype(np.complex64), useful0=u0, seed=seed, bits=w.bits_per_symbol)
+    for fused in (0, 1):
+        cols = [O.Ref.rx_discontinuous(wave, u0, cp, w.N, L, c, win, bool(fused)) for L, c, win in zip(Ls, cs, wins)]
+        out[f"rx_full_{fused}"] = np.concatenate(cols, axis=1).astype(np.complex64)
+    np.savez_compressed(os.path.join(HERE, name + ".npz"), **out)
+    print(name, len(wave))
+
+
 def main():
     if not O.ref_available():
         raise SystemExit("oracle/_ref not built (needs /root/reference)")
@@ -54,6 +83,12 @@ def main():
          [O.design_window(512, n, 4) for n in (288, 288, 288, 408)], O.cp_schedule(15, 2048, 14), rng, qam_bits=4)
     case("g6_30khz_N4096_L16", 4096, [16] * 3, [2464, 2476, 2488], [O.design_window(16, 12, 2)] * 3,
          [352] + [288] * 13 + [352], rng, qam_bits=8)
+    # the hot geometries of BASELINE configs 5 and 4 (the kernels bench.py times)
+    from paper_2008_00672_b200 import configs
+
+    geom = O.Geometry()
+    case_workload("g7_c5_23sb_L256_N4096", configs.config5(geom=geom), 16, 7)
+    case_workload("g8_c4_273sb_L16_N4096", configs.config4(geom=geom), 15, 8)
 
 
 if __name__ == "__main__":

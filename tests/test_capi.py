@@ -170,3 +170,38 @@ def test_workload_geometry():
                 used.append((s.c + ls) % w.N)
         assert len(used) == len(set(used))
         assert (max((u + w.N // 2) % w.N for u in used) - min((u + w.N // 2) % w.N for u in used) + 1) == len(used)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
+def test_workload_geometry_backends_agree(name):
+    """bench.py's reference arm builds every workload from the oracle's geometry
+    (no product library loaded); it must be bit-identical to the product's."""
+    a, b = configs.get(name), configs.get(name, geom=O.Geometry())
+    banks_a = a.banks if hasattr(a, "banks") else [a]
+    banks_b = b.banks if hasattr(b, "banks") else [b]
+    assert len(banks_a) == len(banks_b)
+    for x, y in zip(banks_a, banks_b):
+        assert (x.N, x.cp, x.active_maps, x.bits_per_symbol) == (y.N, y.cp, y.active_maps, y.bits_per_symbol)
+        for s, t in zip(x.subbands, y.subbands):
+            assert (s.L, s.c, s.n_active, s.n_tb, s.l_ofdm) == (t.L, t.c, t.n_active, t.n_tb, t.l_ofdm)
+            assert np.array_equal(np.asarray(s.window).view(np.uint64), np.asarray(t.window).view(np.uint64))
+
+
+def test_nr_cp_schedule_matches_oracle_restatement():
+    for scs, n, B in [(30, 4096, 280), (15, 2048, 28), (60, 4096, 60), (30, 1024, 30)]:
+        assert fb.nr_cp_schedule(fb.make_numerology(scs, n), B).per_symbol_high_rate == O.nr_cp_schedule(scs, n, B)
+    assert O.nr_cp_schedule(30, 4096, 15)[::14] == [352, 352] and O.nr_cp_schedule(30, 4096, 15)[1] == 288
+
+
+def test_configs_import_without_product_library():
+    """Importing the workload definitions with the oracle backend loads no product code."""
+    import subprocess
+    import sys
+
+    code = ("import sys; sys.path.insert(0, %r); import oracle as O; "
+            "from paper_2008_00672_b200 import configs; w = configs.config5(geom=O.Geometry()); "
+            "maps = open('/proc/self/maps').read(); "
+            "assert 'libfcwave_b200' not in maps, 'product library mapped'; "
+            "assert 'paper_2008_00672_b200.api' not in sys.modules; print('ok')" % ROOT)
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr

@@ -24,6 +24,8 @@ CASES = [
     (1024, [256, 256], [200, 700], [100, 257]),
     (2048, [512], [1024], [3000]),  # uniform L >= 512: team-wide short transforms
     (4096, [1024, 1024], [1000, 3000], [2500, 4100]),
+    (1024, [16], [512], [300]),  # narrowband-eligible (config-1 geometry): nb kernels are not used for td I/O
+    (4096, [256], [2048 + 700], [1500]),  # single uniform L = 256
 ]
 
 

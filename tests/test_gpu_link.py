@@ -134,9 +134,11 @@ def test_psd_tone_and_errors():
         api.psd(d, len(t), 1, 64, 1.0)
 
 
-def test_apply_channel_matches_oracle():
-    S, L = 3, 20000
-    d, p = api.exponential_profile(300.0, 20.0, 16)
+@pytest.mark.parametrize("S,n_taps", [(3, 16), (1, 5), (3, 7)])
+def test_apply_channel_matches_oracle(S, n_taps):
+    # odd S * n_taps: the gain table must stay 8-byte aligned in the scratch block
+    L = 20000
+    d, p = api.exponential_profile(300.0, 20.0, n_taps)
     chans = [api.draw_tdl(d, p, 122.88e6, O.derive_seed(4, u)) for u in range(S)]
     rng = np.random.default_rng(6)
     x = (rng.standard_normal((S, L)) + 1j * rng.standard_normal((S, L))).astype(np.complex64)

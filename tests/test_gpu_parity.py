@@ -105,7 +105,54 @@ def _golden():
     return sorted(os.path.join(d, f) for f in os.listdir(d) if f.endswith(".npz"))
 
 
-@pytest.mark.parametrize("path", _golden(), ids=lambda p: os.path.basename(p)[:-4])
+def _hot_golden():
+    return [p for p in _golden() if "packed" in np.load(p).files]
+
+
+@pytest.mark.parametrize("sched", ["default", "chunk1", "chunk7", "static"])
+@pytest.mark.parametrize("path", _hot_golden(), ids=lambda p: os.path.basename(p)[:-4])
+def test_gpu_matches_reference_golden_hot_geometry(path, sched, monkeypatch):
+    """The UNMODIFIED reference's outputs at the exact geometry of BASELINE
+    configs 5 (g7: 23 x L=256, the zero-bin kernel variant) and 4 (g8: 273 x
+    L=16), through the same packed-grid plan and kernels bench.py times, under
+    every work schedule (chunk1 / chunk7: a TX carry recompute at every run
+    start)."""
+    if sched.startswith("chunk"):
+        monkeypatch.setenv("FCW_CHUNK", sched[5:])
+    elif sched == "static":
+        monkeypatch.setenv("FCW_SCHED", "static")
+    z = np.load(path)
+    N, cp = int(z["N"]), z["cp"].tolist()
+    Ls, cs = z["Ls"].tolist(), z["cs"].tolist()
+    wins = np.split(z["windows"], np.cumsum(Ls)[:-1])
+    maps = [m.tolist() for m in np.split(z["active"], np.cumsum(z["n_active"])[:-1])]
+    subs = [api.SubbandConfig(L=L, c=c, window=w) for L, c, w in zip(Ls, cs, wins)]
+    plan = api.Plan(N, cp, subs, maps)
+    S = 3  # three identical units: every unit of a batched launch must match
+    grid = _dev(np.broadcast_to(z["packed"], (S,) + z["packed"].shape))
+    wave = torch.empty((S, plan.Q), dtype=torch.complex64, device="cuda")
+    plan.tx(grid, wave, S)
+    torch.cuda.synchronize()
+    assert plan.Q == len(z["wave"]) and plan.useful0 == int(z["useful0"])
+    got = wave.cpu().numpy()
+    for u in range(S):
+        assert rel_rms(got[u], z["wave"]) <= TOL, (u, rel_rms(got[u], z["wave"]))
+    wref = _dev(np.broadcast_to(z["wave"], (S, len(z["wave"]))))
+    act = np.concatenate([np.asarray(m) + off for m, off in zip(maps, np.cumsum([0] + Ls[:-1]))])
+    for fused in (0, 1):
+        want = z[f"rx_full_{fused}"]
+        out_p = torch.empty((S, len(cp), plan.row_active), dtype=torch.complex64, device="cuda")
+        out_f = torch.empty((S, len(cp), plan.row_full), dtype=torch.complex64, device="cuda")
+        plan.rx(wref, plan.Q, plan.useful0, out_p, S, fused=bool(fused))
+        plan.rx(wref, plan.Q, plan.useful0, out_f, S, fused=bool(fused), full=True)
+        torch.cuda.synchronize()
+        for u in range(S):
+            assert rel_rms(out_f[u].cpu().numpy(), want) <= TOL, (u, fused)
+            assert rel_rms(out_p[u].cpu().numpy(), want[:, act]) <= TOL, (u, fused)
+
+
+@pytest.mark.parametrize("path", [p for p in _golden() if p not in _hot_golden()],
+                         ids=lambda p: os.path.basename(p)[:-4])
 def test_gpu_matches_reference_golden(path):
     """The committed outputs of the UNMODIFIED reference (tests/golden) — full
     DFT-bin grids in, reference waveform / RX columns out."""
@@ -250,6 +297,31 @@ def test_c3_mixed_numerology():
             assert rel_rms(o[u].cpu().numpy(), rp) <= TOL
 
 
+def test_mixed_numerology_zero_fills_uncovered_spans():
+    """Bank order reversed (the 30 kHz bank first, at offset 184): samples
+    [0, 184) and past bank 0's end are only ever ADDED to by bank 1, so the
+    composition must zero them first — the output buffer starts as garbage."""
+    mw = configs.config3()
+    plans = mw.plans()
+    banks = [(plans[1], mw.offsets[1]), (plans[0], mw.offsets[0])]
+    mixed = api.MixedNumerology(banks)
+    S = 2
+    grids = []
+    for i, (w, p) in enumerate(zip(mw.banks, plans)):
+        g = torch.empty((S, w.B, p.row_active), dtype=torch.complex64, device="cuda")
+        p.gen_qam(SEED + i, 0, S, mw.bits_per_symbol, g)
+        grids.append(g)
+    wave = torch.full((S, mixed.Q), 1e3 + 1e3j, dtype=torch.complex64, device="cuda")
+    mixed.tx([grids[1], grids[0]], wave, S)
+    torch.cuda.synchronize()
+    for u in range(S):
+        want = np.zeros(mixed.Q, np.complex128)
+        for (w, p), off, g in zip(zip(mw.banks, plans), mw.offsets, grids):
+            wv, _ = oracle_tx(w, g[u].cpu().numpy().astype(np.complex128))
+            want[off:off + len(wv)] += wv
+        assert rel_rms(wave[u].cpu().numpy(), want) <= TOL
+
+
 def test_tx_accumulate_adds():
     w = truncate(configs.config5(), 16)
     plan = w.plan()
@@ -287,3 +359,59 @@ def test_narrowband_wrapping_span():
             for u in range(S):
                 want_p, _ = oracle_rx(w, wave[u].astype(np.complex128), plan.useful0, fused)
                 assert rel_rms(out[u], want_p) <= TOL, (c, u, fused)
+
+
+# ------------------------------------------------- exported index maps (C ABI)
+@pytest.mark.parametrize("name", ["c1", "c2", "c4", "c5", "random"])
+def test_plan_index_maps_bit_exact(name):
+    """fcw_plan_bin_map / fcw_plan_rx_starts against the oracle's maps
+    (fc_core.cpp:80-84, fc_sync.cpp:148): bit-exact, every subband."""
+    if name == "random":
+        rng = np.random.default_rng(5)
+        subs = [api.SubbandConfig(L=L, c=int(rng.integers(0, 2048)), window=rng.uniform(0, 1, L))
+                for L in (16, 64, 256, 32, 512)]
+        cps = [160, 144, 144, 144]
+        plan, N, cp = api.Plan(2048, cps, subs), 2048, cps
+    else:
+        w = configs.get(name)
+        subs, plan, N, cp = w.subbands, w.plan(), w.N, w.cp
+    for m, s in enumerate(subs):
+        q, b = plan.bin_map(m)
+        oq, ob = O.bin_map(s.L, s.c, N)
+        assert np.array_equal(q, oq) and np.array_equal(b, ob), m
+    for off in (0, 37):
+        u0 = plan.useful0 + off
+        want = O.rx_starts(u0, cp, N, subs[0].L)
+        assert np.array_equal(plan.rx_starts(u0), want)
+    with pytest.raises(IndexError):
+        plan.bin_map(len(subs))
+
+
+@pytest.mark.parametrize("sched", ["default", "chunk1", "chunk7", "static"])
+def test_c4_full_frame(sched, monkeypatch):
+    """All 280 symbols of config 4 (273 x L = 16, NR CP 352 / 288) under every
+    work schedule: TX against the oracle, and fused + direct RX of the
+    oracle's waveform against the oracle."""
+    if sched.startswith("chunk"):
+        monkeypatch.setenv("FCW_CHUNK", sched[5:])
+    elif sched == "static":
+        monkeypatch.setenv("FCW_SCHED", "static")
+    w = configs.config4()
+    plan = w.plan()
+    grid = torch.empty((1, w.B, plan.row_active), dtype=torch.complex64, device="cuda")
+    plan.gen_qam(SEED, 3, 1, w.bits_per_symbol, grid)
+    wave = torch.empty((1, plan.Q), dtype=torch.complex64, device="cuda")
+    plan.tx(grid, wave, 1)
+    torch.cuda.synchronize()
+    key = ("c4full",)
+    if key not in _FULL:
+        ww, u0 = oracle_tx(w, grid[0].cpu().numpy().astype(np.complex128))
+        _FULL[key] = (ww, {f: oracle_rx(w, ww, u0, f)[0] for f in (True, False)})
+    want_w, want_r = _FULL[key]
+    assert rel_rms(wave[0].cpu().numpy(), want_w) <= TOL
+    wref = _dev(want_w[None, :])
+    for f in (True, False):
+        o = torch.empty_like(grid)
+        plan.rx(wref, plan.Q, plan.useful0, o, 1, fused=f)
+        torch.cuda.synchronize()
+        assert rel_rms(o[0].cpu().numpy(), want_r[f]) <= TOL, f

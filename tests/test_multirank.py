@@ -67,3 +67,32 @@ def test_shard_partition_properties():
             assert sum(n for _, n in parts) == total
             assert all(parts[r][0] + parts[r][1] == parts[r + 1][0] for r in range(world - 1))
             assert max(n for _, n in parts) - min(n for _, n in parts) <= 1
+
+
+def test_bench_self_launch_world2_gloo():
+    """`bench.py --gpus 2` outside torchrun spawns 2 ranks itself (127.0.0.1
+    rendezvous), asserts world == --gpus, shards the units and gathers every
+    shard on rank 0 — the multi-GPU control path, on gloo without a GPU."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--dry-run", "--units", "7"],
+                       capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["max_t"] == 2.0
+    assert line["shards"] == [[0, 4], [4, 3]]
+
+
+def test_bench_rejects_world_mismatch():
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "4", "--dry-run"],
+                       capture_output=True, text=True, timeout=120, env=env)
+    assert r.returncode != 0 and "WORLD_SIZE" in (r.stderr + r.stdout)

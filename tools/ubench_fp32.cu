@@ -23,7 +23,7 @@ __global__ void __launch_bounds__(256) fp_kernel(float* out, int reps, float s) 
 }
 
 template <int K>
-void run(const char* name, float* d, int sms) {
+double run(const char* name, float* d, int sms) {
     const int grid = sms * 8, reps = 4096;
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
@@ -41,6 +41,7 @@ void run(const char* name, float* d, int sms) {
     printf("%-28s %.3f ms  %.2f Twarp-instr/s  = %.2f warp-instr/clk/SM at %.0f MHz (%.1f TFLOP/s-equiv x32 lanes)\n", name, ms,
            warp_instr / (ms * 1e-3) / 1e12, warp_instr / (ms * 1e-3) / (clk * 1e3) / sms, clk / 1e3,
            warp_instr * 32 * (K == 0 || K == 1 || K == 4 ? 2 : 1) / (ms * 1e-3) / 1e12);
+    return warp_instr * 32 * (K == 0 || K == 1 || K == 4 ? 2 : 1) / (ms * 1e-3) / 1e12;
 }
 
 int main() {
@@ -48,10 +49,16 @@ int main() {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     float* d;
     cudaMalloc(&d, sms * 8 * 256 * 4);
-    run<0>("FFMA a*b+c (3 reg)", d, sms);
+    const double f0 = run<0>("FFMA a*b+c (3 reg)", d, sms);
     run<1>("FFMA a*imm+imm", d, sms);
     run<2>("FADD", d, sms);
     run<3>("FMUL", d, sms);
-    run<4>("FFMA 3 distinct regs", d, sms);
+    const double f4 = run<4>("FFMA 3 distinct regs", d, sms);
+    int clk;
+    cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+    // the JSON line bench.py reads (profiles/fp32_peak.json): FFMA TFLOP/s (2 flop per lane)
+    printf("{\"ffma_tflops\": %.2f, \"ffma_3distinct_tflops\": %.2f, \"sms\": %d, \"clock_mhz\": %.0f, "
+           "\"how\": \"tools/ubench_fp32.cu: 8 CTAs x 256 thr per SM, 16 independent FFMA chains\"}\n",
+           f0, f4, sms, clk / 1e3);
     return 0;
 }
