@@ -61,16 +61,30 @@ struct Tw {
 };
 
 // --------------------------------------------------------- complex helpers
-FCW_DI float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
-FCW_DI float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+// Complex fp32 arithmetic on the sm_100a packed-FP32 instructions (FADD2 /
+// FMUL2 / FFMA2: one issue slot per complex add / scale, two per complex
+// product, with operand broadcast / swap / negate modifiers).  The FP32 pipe
+// throughput is the same as the scalar forms (tools/ubench_f32x2.cu); what
+// halves is the number of issued instructions, which bounds these kernels.
+// Per component the rounding is that of the scalar code: cmul is
+// (fma(ax, bx, -(ay by)), fma(ax, by, ay bx)) either way.
+FCW_DI float2 cadd(float2 a, float2 b) { return __fadd2_rn(a, b); }
+FCW_DI float2 csub(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
 FCW_DI float2 cmul(float2 a, float2 b) {
-    return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+    return __ffma2_rn(make_float2(a.x, a.x), b, __fmul2_rn(make_float2(a.y, a.y), make_float2(-b.y, b.x)));
 }
 FCW_DI float2 cmulc(float2 a, float2 b) {  // a * conj(b)
-    return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
+    return __ffma2_rn(a, make_float2(b.x, b.x), __fmul2_rn(make_float2(a.y, a.x), make_float2(b.y, -b.y)));
 }
-FCW_DI float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+FCW_DI float2 cscale(float2 a, float s) { return __fmul2_rn(a, make_float2(s, s)); }
 FCW_DI float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
+// a + s * b (real s), one FFMA2
+FCW_DI float2 caxpy(float s, float2 b, float2 a) { return __ffma2_rn(make_float2(s, s), b, a); }
+// a + (p, q) * swap(b) = (a.x + p b.y, a.y + q b.x), one FFMA2: with (p, q) =
+// (-1, 1) it is a + j b, with (1, -1) a - j b
+FCW_DI float2 cswapfma(float2 b, float p, float q, float2 a) {
+    return __ffma2_rn(make_float2(b.y, b.x), make_float2(p, q), a);
+}
 // multiply by j^k (compile-time k)
 template <int K>
 FCW_DI float2 mul_jpow(float2 a) {
@@ -153,30 +167,31 @@ FCW_DI void fft_stage(float2 (&x)[L]) {
                     if constexpr (K != 0) wb = cmul(b, make_float2(Tw<LEN, K, SIGN>::re, Tw<LEN, K, SIGN>::im));
                     x[s + K] = wb;
                     x[s + K + H] = make_float2(-wb.x, -wb.y);  // negation folds into consumers
-                } else if constexpr (K == 0 || 4 * K == LEN) {
-                    // trivial twiddles 1 and -+j: 4 FADD
-                    const float2 wb = (K == 0) ? b : (SIGN < 0 ? make_float2(b.y, -b.x) : make_float2(-b.y, b.x));
-                    x[s + K] = cadd(a, wb);
-                    x[s + K + H] = csub(a, wb);
+                } else if constexpr (K == 0) {
+                    x[s + K] = cadd(a, b);  // FADD2 x 2
+                    x[s + K + H] = csub(a, b);
+                } else if constexpr (4 * K == LEN) {
+                    // trivial twiddle -+j: w b = SIGN < 0 ? -j b : +j b, one FFMA2 per output
+                    constexpr float p = SIGN < 0 ? 1.f : -1.f;
+                    x[s + K] = cswapfma(b, p, -p, a);
+                    x[s + K + H] = cswapfma(b, -p, p, a);
                 } else if constexpr (8 * K == LEN || 8 * K == 3 * LEN) {
-                    // +-45 degree twiddles: w*b = c*(b rotated), 2 FADD + 4 FFMA
+                    // +-45 degree twiddles: w b = c (sr b + si j b), 3 FFMA2
                     constexpr float wr = Tw<LEN, K, SIGN>::re;
                     constexpr float wi = Tw<LEN, K, SIGN>::im;
                     constexpr float c = wr > 0.f ? wr : -wr;
-                    // w = c*(sr + j si) with sr, si in {+1,-1}
                     constexpr float sr = wr > 0.f ? 1.f : -1.f, si = wi > 0.f ? 1.f : -1.f;
-                    const float tr = sr * b.x - si * b.y;
-                    const float ti = si * b.x + sr * b.y;
-                    x[s + K] = make_float2(fmaf(c, tr, a.x), fmaf(c, ti, a.y));
-                    x[s + K + H] = make_float2(fmaf(-c, tr, a.x), fmaf(-c, ti, a.y));
+                    // t = sr b + si j b = (sr b.x - si b.y, sr b.y + si b.x)
+                    const float2 t = cswapfma(b, -si, si, make_float2(sr * b.x, sr * b.y));
+                    x[s + K] = caxpy(c, t, a);
+                    x[s + K + H] = caxpy(-c, t, a);
                 } else {
-                    // general twiddle: y0 = a + w b (4 FFMA), y1 = 2a - y0 (2 FFMA)
+                    // general twiddle: y0 = a + w b (2 FFMA2), y1 = 2a - y0 (1 FFMA2)
                     constexpr float wr = Tw<LEN, K, SIGN>::re;
                     constexpr float wi = Tw<LEN, K, SIGN>::im;
-                    const float y0r = fmaf(wr, b.x, fmaf(-wi, b.y, a.x));
-                    const float y0i = fmaf(wr, b.y, fmaf(wi, b.x, a.y));
-                    x[s + K] = make_float2(y0r, y0i);
-                    x[s + K + H] = make_float2(fmaf(2.f, a.x, -y0r), fmaf(2.f, a.y, -y0i));
+                    const float2 y0 = caxpy(wr, b, cswapfma(b, -wi, wi, a));
+                    x[s + K] = y0;
+                    x[s + K + H] = __ffma2_rn(make_float2(2.f, 2.f), a, make_float2(-y0.x, -y0.y));
                 }
             }
             fft_stage<L, SIGN, LEN, K + 1, ZM, OM>(x);
