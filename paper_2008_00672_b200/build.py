@@ -119,6 +119,8 @@ if __name__ == "__main__":
         i = sys.argv.index("--variant")
         name, defs = sys.argv[i + 1], sys.argv[i + 2].split(",") if len(sys.argv) > i + 2 else []
         srcs = sys.argv[i + 3].split(",") if len(sys.argv) > i + 3 else ["fcw_k_n4096b.cu"]
+        if srcs == ["ALL"]:
+            srcs = list(SOURCES_CU)
         print(build_variant(name, [d for d in defs if d], srcs))
     else:
         print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -39,6 +39,17 @@ constexpr int kPPT = 16;  // long-transform points per thread and block
 #endif
 #define FCW_SKIP(P, bit) (FCW_DEV_KNOBS && ((P).dbg_skip & (bit)))
 
+// Bounds checks of every computed SMEM / global index on the hot path
+// (the `check` library variant, tools/checked_run.sh; compute-sanitizer is
+// not available on the GPU pool).  A failed check traps the kernel.
+#ifndef FCW_CHECK
+#define FCW_CHECK 0
+#endif
+#define FCW_ASSERT(c)                        \
+    do {                                     \
+        if (FCW_CHECK && !(c)) __trap();     \
+    } while (0)
+
 // Bin-class entry (plan, per class and DFT bin b), 8 bytes:
 //   x = (inv[b] & 0xffff) | sec(p0) << 16, y = bits(w[p0]), p0 = b ^ L/2;
 //   sec = -2: zero weight (no contribution), -1: primary (spectrum slot q),
@@ -184,6 +195,7 @@ FCW_DI void tx_short_thread(const KParams& P, const Team& tm, const SymDev& sy, 
         for (int b = 0; b < L; ++b) {
             const Bin e = bin_entry<N, L>(P, sd, b);
             if (e.dest >= 0) {
+                FCW_ASSERT(e.dest < P.spec_stride);
                 spec0[e.dest] = cscale(u0[b], e.w);
                 spec1[e.dest] = cscale(u1[b], e.w * sd.bp1);
             }
@@ -271,6 +283,7 @@ FCW_DI void tx_short_warp_lockstep(const KParams& P, const Team& tm, const SymDe
             constexpr int K = decltype(kc)::value;
             const BinW e = bin_warp<N, L, K>(ent[K], qbase, ext0);
             if (e.dest >= 0) {
+                FCW_ASSERT(e.dest < P.spec_stride);
                 spec0[e.dest] = cscale(uu[0][K], e.w);
                 spec1[e.dest] = cscale(uu[1][K], e.w * bp1);
             }
@@ -393,6 +406,7 @@ FCW_DI void tx_short_warp(const KParams& P, const Team& tm, const SymDev& sy, co
             static_for<PPT>([&](auto kc) {
                 constexpr int K = decltype(kc)::value;
                 const BinW e = bin_warp<N, L, K>(__ldg(&ce[32 * K]), qbase, ext0);
+                FCW_ASSERT(e.dest < P.spec_stride);
                 if (e.dest >= 0) spec[e.dest] = cscale(uu[r][K], e.w * sgn);
             });
         }
@@ -464,8 +478,10 @@ FCW_DI void tx_short_half(const KParams& P, const Team& tm, const SymDev& sy, co
             } else {
                 const float2* g = row + sd.act_off;
 #pragma unroll
-                for (int k = 0; k < PPT; ++k)
+                for (int k = 0; k < PPT; ++k) {
+                    FCW_ASSERT(!act || sd.act_off + inv[k] < P.row_len);
                     if (live(k)) v[k] = ld_stream(g + max(inv[k], 0));
+                }
 #pragma unroll
                 for (int k = 0; k < PPT; ++k)
                     if (live(k)) v[k] = inv[k] >= 0 ? v[k] : zero2();
@@ -504,6 +520,7 @@ FCW_DI void tx_short_half(const KParams& P, const Team& tm, const SymDev& sy, co
                     const int2 e = __ldg(&ce[TW * K]);
                     const int sec = e.x >> 16;
                     const int dest = sec >= 0 ? ext0 + sec : (sec == -1 ? ((qbase + TW * KP) & (N - 1)) : -1);
+                    FCW_ASSERT(dest < P.spec_stride);
                     if (act && dest >= 0) spec[dest] = cscale(u[K], __int_as_float(e.y) * sgn);
                 }
             });
@@ -599,6 +616,7 @@ FCW_DI void tx_short_lanes16(const KParams& P, const Team& tm, const SymDev& sy,
         if (!((b >= L / 4) && (b < 3 * L / 4))) u[1] = zero2();
         lane_fft16<N, -1, 2>(u, b, P.tw);
         if (act && e.dest >= 0) {
+            FCW_ASSERT(e.dest < P.spec_stride);
             spec0[e.dest] = cscale(u[0], e.w);
             spec1[e.dest] = cscale(u[1], e.w * sd.bp1);
         }
@@ -691,6 +709,7 @@ FCW_DI void tx_short_team(const KParams& P, const Team& tm, const SymDev& sy, co
         for (int k = 0; k < PPT; ++k) {
             const Bin e = bin_entry<N, L>(P, sd, t + TT * k);
             if (e.dest >= 0) {
+                FCW_ASSERT(e.dest < P.spec_stride);
                 spec0[e.dest] = cscale(uu[0][k], e.w);
                 spec1[e.dest] = cscale(uu[1][k], e.w * sd.bp1);
             }
@@ -998,7 +1017,10 @@ FCW_DI void rx_short_warp(const KParams& P, const Team& tm, const SymDev& sy, co
             float2* o = orow + sd.act_off;
 #pragma unroll
             for (int k = 0; k < PPT; ++k)
-                if (inv[k] >= 0) o[inv[k]] = g0[0][k];
+                if (inv[k] >= 0) {
+                    FCW_ASSERT(sd.act_off + inv[k] < P.row_len);
+                    o[inv[k]] = g0[0][k];
+                }
         }
         __syncwarp();
     }
@@ -1075,6 +1097,7 @@ FCW_DI void rx_short_half(const KParams& P, const Team& tm, const SymDev& sy, co
 #pragma unroll
                 for (int k = 0; k < PPT; ++k)
                     if (!((ZO >> k) & 1ull) && inv[k] >= 0) {
+                        FCW_ASSERT(sd.act_off + inv[k] < P.row_len);
                         __stcs(&o[inv[k]], outv(k));  // streaming store: the grid is not re-read here
                     }
             }
@@ -1401,6 +1424,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) tx_kernel(const KP
             // rank of secondary contributions (disjoint bins: one barrier less)
             for (int k = gtid; k < P.n_zero; k += TT) {
                 const int q = __ldg(&P.zero_list[k]);
+                FCW_ASSERT(q >= 0 && q < P.spec_stride);
                 spec0[q] = zero2();
                 spec1[q] = zero2();
             }
@@ -1408,6 +1432,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) tx_kernel(const KP
             for (int l = 0; l < P.n_lvl; ++l) {
                 for (int k = P.lvl_start[l] + gtid; k < P.lvl_start[l + 1]; k += TT) {
                     const int q = __ldg(&P.fix_tgt[k]), e = N + __ldg(&P.fix_slot[k]);
+                    FCW_ASSERT(q >= 0 && q < N && e < P.spec_stride);
                     spec0[q] = cadd(spec0[q], spec0[e]);
                     spec1[q] = cadd(spec1[q], spec1[e]);
                 }
@@ -1460,10 +1485,12 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) tx_kernel(const KP
                     if (mm < 8) val = cadd(val, cr[mm]);
                     if (u < sy.own_len) {
                         if (emit) {
+                            FCW_ASSERT(sy.sigma + u < P.Q);
                             if (P.accumulate) dst[u] = cadd(dst[u], val);
                             else __stcs(&dst[u], val);  // streaming: the waveform is not re-read here (-1.4%)
                         }
                     } else {
+                        FCW_ASSERT(u - sy.own_len < N / 2);
                         carry[u - sy.own_len] = val;
                     }
                 }
@@ -1522,6 +1549,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) rx_kernel(const KP
                 }
             } else if (act) {
                 // rx_segment (fc_sync.cpp:145-156): y0 = w[start, +N), y1 = w[start + N/2, +N)
+                FCW_ASSERT(P.rx_base + sy.sigma >= 0 && P.rx_base + sy.sigma + 3 * N / 2 <= P.wave_len);
                 const float2* src = in_u + P.rx_base + sy.sigma + gtid;
 #pragma unroll
                 for (int mm = 0; mm < 24; ++mm) {
