@@ -804,6 +804,9 @@ FCW_DI void tx_short_all(const KParams& P, const Team& tm, const SymDev& sy, con
                          float2* scr, const float2* stw) {
     if constexpr (ZV == 2 && LU == 16) {
         tx_short_lanes16<N>(P, tm, sy, row, spec0, spec1);
+    } else if constexpr (ZV == 3 && use_team_short<N, LU>()) {
+        // team-only kernels: the plan has at most one subband per two warps
+        tx_short_team<N, LU, teams_per_cta<N>()>(P, tm, sy, row, spec0, spec1, scr);
     } else if constexpr (use_team_short<N, LU>()) {
         // few subbands: the whole team per subband; else one warp per subband
         if (2 * P.M <= tm.nwarp)
@@ -1131,6 +1134,11 @@ FCW_DI void rx_short_all(const KParams& P, const Team& tm, const SymDev& sy, con
             rx_short_lanes16<N>(P, tm, sy, spec0, spec1, orow);
         else
             rx_short_one<N, LU>(P, tm, sy, spec0, spec1, orow, scr, stw, 0, P.M);
+    } else if constexpr (ZV == 3 && use_team_short<N, LU>()) {
+        if (P.fused)
+            rx_short_team<N, LU, teams_per_cta<N>(), true>(P, tm, sy, spec0, spec1, orow, scr);
+        else
+            rx_short_team<N, LU, teams_per_cta<N>(), false>(P, tm, sy, spec0, spec1, orow, scr);
     } else if constexpr (use_team_short<N, LU>()) {
         if (2 * P.M > tm.nwarp)
             rx_short_one<N, LU>(P, tm, sy, spec0, spec1, orow, scr, stw, 0, P.M);
@@ -1161,8 +1169,11 @@ FCW_DI void rx_short_all(const KParams& P, const Team& tm, const SymDev& sy, con
 
 // ------------------------------------------------------------------ kernels
 
-template <int LU>
+template <int LU, int ZV = 0>
 constexpr int min_blocks() {
+    // ZV = 3 (team-only short path, few L >= 512 subbands: 4-8 points per
+    // thread): two CTAs per SM at <= 128 registers
+    if (ZV == 3) return 2;
     // L >= 512: the warp paths hold 16-32 points per lane; one CTA per SM with
     // up to 255 registers beats two spilling CTAs (config 2: 30 -> 38 Gsamples/s)
     if (LU >= 512) return 1;
@@ -1367,7 +1378,7 @@ FCW_DI Smem smem_layout(const KParams& P, int g) {
 }
 
 template <int N, int LU, bool DYN, int ZV = 0>
-__global__ void __launch_bounds__(kThreads, min_blocks<LU>()) tx_kernel(const KParams P) {
+__global__ void __launch_bounds__(kThreads, min_blocks<LU, ZV>()) tx_kernel(const KParams P) {
     constexpr int G = teams_per_cta<N>();
     constexpr int T = N / kPPT;                  // long-transform threads per team
     constexpr int TT = G == 1 ? kThreads : T;    // threads per team
@@ -1500,7 +1511,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) tx_kernel(const KP
 }
 
 template <int N, int LU, bool DYN, int ZV = 0>
-__global__ void __launch_bounds__(kThreads, min_blocks<LU>()) rx_kernel(const KParams P) {
+__global__ void __launch_bounds__(kThreads, min_blocks<LU, ZV>()) rx_kernel(const KParams P) {
     constexpr int G = teams_per_cta<N>();
     constexpr int T = N / kPPT;
     constexpr int TT = G == 1 ? kThreads : T;
@@ -1537,7 +1548,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU>()) rx_kernel(const KP
             if (gtid == 0 && n + 1 < n1) prefetch_l2(in_u + P.rx_base + P.sym[n + 1].sigma, 8LL * (3 * N / 2));
             float2 v[2][kPPT];
             bool bounded = false;  // continuous FC: zeros outside [0, wave_len) (rx_continuous pads)
-            if constexpr (ZV == 0) bounded = P.td != nullptr;
+            if constexpr (ZV == 0 || ZV == 3) bounded = P.td != nullptr;
             if (act && bounded) {
                 const long long j0 = P.rx_base + sy.sigma + gtid;
 #pragma unroll

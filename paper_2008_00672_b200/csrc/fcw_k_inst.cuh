@@ -26,3 +26,12 @@
         return KernelPair{tx_kernel<NN, LL, false, 2>, rx_kernel<NN, LL, false, 2>,              \
                           tx_kernel<NN, LL, true, 2>, rx_kernel<NN, LL, true, 2>};               \
     }
+
+// ... and the team-only variant (ZV = 3: uniform L >= 512 with at most one
+// subband per two warps of a team, e.g. config 3's banks): the whole team
+// transforms each subband at 4-8 points per thread, two CTAs per SM.
+#define FCW_KERNELS_NLT(NN, LL)                                                                   \
+    KernelPair kernels_n##NN##_l##LL##t() {                                                       \
+        return KernelPair{tx_kernel<NN, LL, false, 3>, rx_kernel<NN, LL, false, 3>,              \
+                          tx_kernel<NN, LL, true, 3>, rx_kernel<NN, LL, true, 3>};               \
+    }

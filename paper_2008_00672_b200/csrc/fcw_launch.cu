@@ -42,6 +42,11 @@ KernelPair kernels_n4096_l512();
 KernelPair kernels_n4096_l1024();
 KernelPair kernels_n4096_l256z();
 KernelPair kernels_n1024_l16n();
+KernelPair kernels_n4096_l1024t();
+KernelPair kernels_n2048_l512t();
+KernelPair kernels_n2048_l1024t();
+KernelPair kernels_n1024_l512t();
+KernelPair kernels_n1024_l1024t();
 
 namespace {
 
@@ -66,8 +71,15 @@ KernelPair pick_l(int N, int LU) {
 #undef FCW_PICK_L
 }
 
-KernelPair pick(int N, int LU, bool zv = false, bool nb = false) {
+KernelPair pick(int N, int LU, bool zv = false, bool nb = false, bool team = false) {
     if (zv && N == 4096 && LU == 256) return kernels_n4096_l256z();
+    if (team) {
+        if (N == 4096 && LU == 1024) return kernels_n4096_l1024t();
+        if (N == 2048 && LU == 512) return kernels_n2048_l512t();
+        if (N == 2048 && LU == 1024) return kernels_n2048_l1024t();
+        if (N == 1024 && LU == 512) return kernels_n1024_l512t();
+        if (N == 1024 && LU == 1024) return kernels_n1024_l1024t();
+    }
     if (nb && N == 1024 && LU == 16) return kernels_n1024_l16n();
     switch (N) {
         case 16: return kernels_n16_l0();
@@ -87,6 +99,17 @@ int uniform_L(const Plan& p) {
     return (L >= 16 && L <= 1024) ? L : 0;
 }
 
+// Team-only kernels (ZV = 3): uniform L >= 512 with the team-wide short path
+// usable (>= 4 points per thread) and at most one subband per two warps of a
+// team (use_team_short / tx_short_all in fcw_device.cuh).
+bool team_only(const Plan& p) {
+    const int LU = uniform_L(p);
+    if (LU < 512) return false;  // (continuous TX plans with L >= 512 run the generic kernels: LU = 0)
+    const int G = (p.N >= 512 && p.N <= 4096) ? 4096 / p.N : 1, TT = G == 1 ? kThreads : p.N / kPPT;
+    if (LU > p.N || LU / TT < 4) return false;
+    return 2 * p.M <= TT / 32;
+}
+
 // RX with the half-warp L = 256 path keeps a wrap-around copy of bins [0, L)
 // at [N, N + L) (rx_kernel, rx_short_half).
 bool rx_mirror(const Plan& p) { return uniform_L(p) == 256; }
@@ -104,8 +127,15 @@ int spec_stride(const Plan& p, bool mirror = false) {
 // RX: one buffer, two where the direct path needs both blocks' short outputs
 // at once (L = 64, generic plans).
 int scratch_one(const Plan& p) { return (p.Lmax + p.Lmax / 16 + 2 + 1) & ~1; }
+bool team_only(const Plan& p);
 int scratch_stride(const Plan& p, int LU, bool tx, bool rx_direct) {
     if (p.Lmax < 64) return 0;
+    if (team_only(p)) {
+        // tx/rx_short_team: two buffers of L + L/16 + 2 per team, spread over
+        // the team's contiguous warp scratch
+        const int wpt = (p.N >= 512 && p.N <= 4096) ? kWarps / (4096 / p.N) : kWarps;
+        return ((2 * (p.Lmax + p.Lmax / 16 + 2) + wpt - 1) / wpt + 1) & ~1;
+    }
     if (tx) return 2 * scratch_one(p);
     // fused L = 256 runs on half-warps: one buffer per half
     const bool two = (rx_direct && (LU == 0 || LU == 64 || p.Lmax == 64)) || p.Lmax == 256;
@@ -283,7 +313,7 @@ cudaError_t launch_tx(const Plan& p, KParams& kp, int S, cudaStream_t st) {
     kp.n_units = S;
     kp.teams = teams(p);
     kp.n_items = S * kp.nchunks;
-    const KernelPair kp2 = pick(p.N, LU, p.zv, p.nb);
+    const KernelPair kp2 = pick(p.N, LU, p.zv, p.nb, team_only(p));
     return launch_one(kp.dynamic ? kp2.tx_d : kp2.tx, smem_bytes(p, true, false), kp, true, p.N, teams(p), st);
 }
 
@@ -295,7 +325,7 @@ cudaError_t launch_rx(const Plan& p, KParams& kp, int S, cudaStream_t st) {
     kp.n_units = S;
     kp.teams = teams(p);
     kp.n_items = S * kp.nchunks;
-    const KernelPair kp2 = pick(p.N, LU, p.zv, p.nb);
+    const KernelPair kp2 = pick(p.N, LU, p.zv, p.nb, team_only(p));
     return launch_one(kp.dynamic ? kp2.rx_d : kp2.rx, smem_bytes(p, false, direct), kp, false, p.N, teams(p), st);
 }
 
