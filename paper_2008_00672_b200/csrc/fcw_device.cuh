@@ -121,6 +121,13 @@ FCW_DI int theta_exp(int cmodN, int smodN) {
 
 FCW_DI float2 zero2() { return make_float2(0.f, 0.f); }
 
+// *p += v as one fire-and-forget L2 reduction (red.global.add.v2.f32, sm_90+):
+// FCW_TX_ACCUMULATE adds each sample exactly once onto the stored waveform,
+// so the result equals the load-add-store it replaces, bit for bit.
+FCW_DI void red_add2(float2* p, float2 v) {
+    asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(v.x), "f"(v.y) : "memory");
+}
+
 constexpr int kLtwLen = 64 + 4096 / 64;  // two-level long-transform twiddles (SMEM)
 constexpr int kTw16Len = 512;            // fft256_half per-lane twiddles (uniform L = 256 kernels)
 #ifndef FCW_TX_TAIL2
@@ -1420,8 +1427,6 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU, ZV>()) tx_kernel(cons
             team_sync<G>(g, TT);  // previous symbol's transform no longer reads spec
             if (gtid == 0 && n + 1 < n1) {
                 prefetch_l2(in_u + (long long)(n + 1) * P.row_len, 8LL * P.row_len);
-                // FCW_TX_ACCUMULATE reads the waveform it adds to: bring the next symbol's span in too
-                if (P.accumulate) prefetch_l2(out_u + P.sym[n + 1].sigma, 8LL * (3 * N / 2));
             }
             if (!FCW_SKIP(P, 1)) {
                 // time-domain input (continuous FC, ZV == 0 kernels only) stages within a symbol only
@@ -1497,7 +1502,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU, ZV>()) tx_kernel(cons
                     if (u < sy.own_len) {
                         if (emit) {
                             FCW_ASSERT(sy.sigma + u < P.Q);
-                            if (P.accumulate) dst[u] = cadd(dst[u], val);
+                            if (P.accumulate) red_add2(&dst[u], val);  // L2-side add, no load latency
                             else __stcs(&dst[u], val);  // streaming: the waveform is not re-read here (-1.4%)
                         }
                     } else {
