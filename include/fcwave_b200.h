@@ -131,6 +131,51 @@ int fcw_tx(const fcw_plan* plan, const void* grid, int64_t grid_unit_stride, voi
 int fcw_rx(const fcw_plan* plan, const void* wave, int64_t wave_unit_stride, int64_t wave_len,
            int64_t useful0, void* grid, int64_t grid_unit_stride, int S, unsigned flags, void* stream);
 
+/* ------------------- reference-granularity per-symbol entry points
+ * The reference's finer hot-path API (fc_sync.hpp:38-75), batched over S
+ * items (units) of ONE (subband m, symbol n) of the plan, on the device, in
+ * complex fp32 (all buffers device complex64; a stride of 0 = contiguous).
+ * They run their own generic kernels (fcw_symbol.cu), not the fused
+ * whole-frame K-TX / K-RX; use fcw_tx / fcw_rx for throughput. */
+
+/* symbol_phase (fc_sync.hpp:24, fc_sync.cpp:45-50) and block_phase
+ * (fc_core.cpp:41-44) in double, bit-exact with the reference. */
+int fcw_symbol_phase(int n, int c, const int* cp_high, int B, int N, double* re, double* im);
+int fcw_block_phase(int64_t r, int c, int L_S, int L, double* re, double* im);
+
+/* tx_symbol (fc_sync.hpp:41-42): sym [S][sym_stride] holds the CP-OFDM
+ * symbol n of subband m, L + l_cp samples (l_cp <= L_L); out [S][out_stride]
+ * receives its 3N/2 filtered samples (FilteredSymbol::samples). */
+int fcw_tx_symbol(const fcw_plan* plan, int m, int n, const void* sym, int64_t sym_stride, int l_cp, void* out,
+                  int64_t out_stride, int S, void* stream);
+
+/* combine_symbols (fc_sync.hpp:46-47): syms [S][B][3N/2] (symbol n at index
+ * n, unit stride sym_unit_stride, 0 = B*3N/2) overlap-added at sigma_n into
+ * wave [S][wave_stride] (Q samples, useful0 = N_L). */
+int fcw_combine_symbols(const fcw_plan* plan, const void* syms, int64_t sym_unit_stride, void* wave,
+                        int64_t wave_stride, int S, void* stream);
+
+/* rx_segment (fc_sync.hpp:60): y0 = w[start, +N), y1 = w[start + N/2, +N),
+ * start = useful0 - N_L + sigma_n, for S waveforms.  FCW_ERANGE for n outside
+ * the CP schedule, FCW_EINVAL when the window leaves the waveform. */
+int fcw_rx_segment(const fcw_plan* plan, const void* wave, int64_t wave_stride, int64_t wave_len, int64_t useful0,
+                   int n, void* y0, void* y1, int64_t y_stride, int S, void* stream);
+
+/* rx_block_freq (fc_sync.hpp:73): g [S][g_stride] = the L frequency-domain FC
+ * outputs of subband m of the N-sample blocks y [S][y_stride], with phase. */
+int fcw_rx_block_freq(const fcw_plan* plan, int m, const void* y, int64_t y_stride, double phase_re,
+                      double phase_im, void* g, int64_t g_stride, int S, void* stream);
+
+/* rx_symbol_simplified (fc_sync.hpp:69-70), Eq. (30): L bins of subband m
+ * from g0, g1 [S][g_stride]. */
+int fcw_rx_symbol_simplified(const fcw_plan* plan, int m, const void* g0, const void* g1, int64_t g_stride,
+                             void* out, int64_t out_stride, int S, void* stream);
+
+/* rx_symbol_direct (fc_sync.hpp:64-65): L bins of subband m, symbol n, from
+ * the blocks y0, y1 [S][y_stride]. */
+int fcw_rx_symbol_direct(const fcw_plan* plan, int m, int n, const void* y0, const void* y1, int64_t y_stride,
+                         void* out, int64_t out_stride, int S, void* stream);
+
 /* Seeded synthetic QAM grid on the device, bit-identical to the host oracle:
  * per unit u a splitmix64 stream seeded derive_seed(seed, unit0 + u)
  * (channel.cpp:19-48), one draw per bit LSB-first (scenario.cpp:110-128),

@@ -11,7 +11,7 @@ _API = (
     "CpSchedule", "FcParams", "Numerology", "PinnedBuffer", "Plan", "QamGrid", "SubbandConfig", "Waveform",
     "centered_active_map", "combined_length", "cp_schedule", "cp_truncate", "derive_fc_params", "design_window",
     "first_block_overlap", "make_numerology", "nr_cp_schedule", "rx_discontinuous", "rx_discontinuous_all",
-    "symbol_sigma", "tx_discontinuous",
+    "symbol_sigma", "tx_discontinuous", "symbol_phase", "block_phase",
 )
 __all__ = list(_API) + ["FcwError"]
 __version__ = "0.1.0"

@@ -29,7 +29,8 @@ EXPORTS = [
     "fcw_centered_active_map", "fcw_symbol_sigma", "fcw_combined_length", "fcw_last_error", "fcw_version",
     "fcw_link_stats", "fcw_awgn", "fcw_wave_power", "fcw_psd", "fcw_draw_tdl", "fcw_apply_channel",
     "fcw_cont_plan_create", "fcw_cont_plan_destroy", "fcw_cont_plan_get_info", "fcw_tx_continuous",
-    "fcw_rx_continuous", "fcw_wave_zero",
+    "fcw_rx_continuous", "fcw_wave_zero", "fcw_symbol_phase", "fcw_block_phase", "fcw_tx_symbol",
+    "fcw_combine_symbols", "fcw_rx_segment", "fcw_rx_block_freq", "fcw_rx_symbol_simplified", "fcw_rx_symbol_direct",
 ]
 
 
@@ -108,6 +109,15 @@ def lib() -> C.CDLL:
     L.fcw_draw_tdl.argtypes = [vp, vp, C.c_int, C.c_double, C.c_uint64, vp, vp]
     L.fcw_apply_channel.argtypes = [vp, vp, i64, i64, C.c_int, vp, vp, C.c_int, vp]
     L.fcw_wave_zero.argtypes = [vp, i64, C.c_int, i64, i64, vp]
+    dp = C.POINTER(C.c_double)
+    L.fcw_symbol_phase.argtypes = [C.c_int, C.c_int, i32p, C.c_int, C.c_int, dp, dp]
+    L.fcw_block_phase.argtypes = [i64, C.c_int, C.c_int, C.c_int, dp, dp]
+    L.fcw_tx_symbol.argtypes = [vp, C.c_int, C.c_int, vp, i64, C.c_int, vp, i64, C.c_int, vp]
+    L.fcw_combine_symbols.argtypes = [vp, vp, i64, vp, i64, C.c_int, vp]
+    L.fcw_rx_segment.argtypes = [vp, vp, i64, i64, i64, C.c_int, vp, vp, i64, C.c_int, vp]
+    L.fcw_rx_block_freq.argtypes = [vp, C.c_int, vp, i64, C.c_double, C.c_double, vp, i64, C.c_int, vp]
+    L.fcw_rx_symbol_simplified.argtypes = [vp, C.c_int, vp, vp, i64, vp, i64, C.c_int, vp]
+    L.fcw_rx_symbol_direct.argtypes = [vp, C.c_int, C.c_int, vp, vp, i64, vp, i64, C.c_int, vp]
     L.fcw_psd.argtypes = [vp, i64, i64, C.c_int, C.c_int, C.c_double, C.POINTER(C.c_double), vp]
     L.fcw_cont_plan_create.argtypes = [C.POINTER(vp), C.c_int, C.c_double, vp, C.c_int, C.POINTER(C.c_int64), i64,
                                        C.c_int]

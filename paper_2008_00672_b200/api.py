@@ -155,6 +155,21 @@ def centered_active_map(l_ofdm: int, n_active: int, skip_dc: bool = True) -> lis
     return b[:n_active].tolist()
 
 
+def symbol_phase(n: int, c: int, cps: CpSchedule, N: int) -> complex:
+    """symbol_phase (fc_sync.cpp:45-50), double precision."""
+    cp = _i32(cps.per_symbol_high_rate)
+    a, b = C.c_double(), C.c_double()
+    check(lib().fcw_symbol_phase(n, c, _i32p(cp), len(cp), N, C.byref(a), C.byref(b)))
+    return complex(a.value, b.value)
+
+
+def block_phase(r: int, c: int, L_S: int, L: int) -> complex:
+    """block_phase (fc_core.cpp:41-44), double precision."""
+    a, b = C.c_double(), C.c_double()
+    check(lib().fcw_block_phase(r, c, L_S, L, C.byref(a), C.byref(b)))
+    return complex(a.value, b.value)
+
+
 def symbol_sigma(n: int, cps: CpSchedule, N: int) -> int:
     cp = _i32(cps.per_symbol_high_rate)
     return int(lib().fcw_symbol_sigma(n, _i32p(cp), N))
@@ -290,6 +305,44 @@ class Plan:
 
     def gen_qam(self, seed: int, unit0: int, S: int, bits_per_symbol: int, grid, stream=None) -> None:
         check(lib().fcw_gen_qam(self._h, seed, unit0, S, bits_per_symbol, _dev_ptr(grid), _stream_ptr(stream)))
+
+    # -- reference-granularity per-symbol entry points (fc_sync.hpp:38-75),
+    #    batched over S units of one (subband m, symbol n); device buffers
+    def tx_symbol(self, m: int, n: int, sym, l_cp: int, out, S: int, stream=None, sym_stride: int = 0,
+                  out_stride: int = 0) -> None:
+        """tx_symbol (fc_sync.cpp:60-84): sym [S][L + l_cp] -> out [S][3N/2]."""
+        check(lib().fcw_tx_symbol(self._h, m, n, _dev_ptr(sym), sym_stride, l_cp, _dev_ptr(out), out_stride, S,
+                                  _stream_ptr(stream)))
+
+    def combine_symbols(self, syms, wave, S: int, stream=None, sym_unit_stride: int = 0,
+                        wave_stride: int = 0) -> None:
+        """combine_symbols (fc_sync.cpp:96-112): syms [S][B][3N/2] -> wave [S][Q]."""
+        check(lib().fcw_combine_symbols(self._h, _dev_ptr(syms), sym_unit_stride, _dev_ptr(wave), wave_stride, S,
+                                        _stream_ptr(stream)))
+
+    def rx_segment(self, wave, wave_len: int, useful0: int, n: int, y0, y1, S: int, stream=None,
+                   wave_stride: int = 0, y_stride: int = 0) -> None:
+        """rx_segment (fc_sync.cpp:145-156): the two N-sample blocks of symbol n."""
+        check(lib().fcw_rx_segment(self._h, _dev_ptr(wave), wave_stride, wave_len, useful0, n, _dev_ptr(y0),
+                                   _dev_ptr(y1), y_stride, S, _stream_ptr(stream)))
+
+    def rx_block_freq(self, m: int, y, phase: complex, g, S: int, stream=None, y_stride: int = 0,
+                      g_stride: int = 0) -> None:
+        """rx_block_freq (fc_sync.cpp:178-193): y [S][N] -> g [S][L_m]."""
+        check(lib().fcw_rx_block_freq(self._h, m, _dev_ptr(y), y_stride, float(phase.real), float(phase.imag),
+                                      _dev_ptr(g), g_stride, S, _stream_ptr(stream)))
+
+    def rx_symbol_simplified(self, m: int, g0, g1, out, S: int, stream=None, g_stride: int = 0,
+                             out_stride: int = 0) -> None:
+        """rx_symbol_simplified (fc_sync.cpp:195-243), Eq. (30): g0, g1 [S][L] -> out [S][L]."""
+        check(lib().fcw_rx_symbol_simplified(self._h, m, _dev_ptr(g0), _dev_ptr(g1), g_stride, _dev_ptr(out),
+                                             out_stride, S, _stream_ptr(stream)))
+
+    def rx_symbol_direct(self, m: int, n: int, y0, y1, out, S: int, stream=None, y_stride: int = 0,
+                         out_stride: int = 0) -> None:
+        """rx_symbol_direct (fc_sync.cpp:158-176): y0, y1 [S][N] -> out [S][L]."""
+        check(lib().fcw_rx_symbol_direct(self._h, m, n, _dev_ptr(y0), _dev_ptr(y1), y_stride, _dev_ptr(out),
+                                         out_stride, S, _stream_ptr(stream)))
 
     # -- host entry points (numpy complex64, C-contiguous)
     # ---- link step around the path (SURVEY §8 f1/f3)

@@ -24,7 +24,7 @@ NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-r
               "-Xptxas", "-v", "-I", os.path.join(ROOT, "include"), "-I", CSRC]
 CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-Wall", "-Wextra", "-I", os.path.join(ROOT, "include"), "-I", CSRC]
 
-SOURCES_CU = ["fcw_launch.cu", "fcw_link.cu", "fcw_cont.cu", "fcw_k_small.cu", "fcw_k_n4096z.cu", "fcw_k_n1024n.cu", "fcw_k_team.cu"] + [f"fcw_k_n{n}{g}.cu" for n in (4096, 2048, 1024) for g in "bcag"]
+SOURCES_CU = ["fcw_launch.cu", "fcw_link.cu", "fcw_cont.cu", "fcw_k_small.cu", "fcw_k_n4096z.cu", "fcw_k_n1024n.cu", "fcw_k_team.cu", "fcw_symbol.cu"] + [f"fcw_k_n{n}{g}.cu" for n in (4096, 2048, 1024) for g in "bcag"]
 SOURCES_CPP = ["fcw_capi.cpp", "fcw_host.cpp"]
 
 

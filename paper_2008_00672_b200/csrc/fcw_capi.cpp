@@ -751,6 +751,175 @@ int fcw_rx(const fcw_plan* p, const void* wave, int64_t wave_stride, int64_t wav
     return FCW_OK;
 }
 
+// ----------------------------------------------- per-symbol entry points
+namespace {
+constexpr double kTwoPi = 6.283185307179586476925286766559;
+
+// symbol_phase (fc_sync.cpp:45-50): exp(+j 2 pi ((c mod N)(S_n mod N) mod N) / N)
+void symbol_phase_d(int n, int c, const std::vector<int>& cp, int N, double* re, double* im) {
+    long long sn = 0;
+    for (int q = 1; q <= n; ++q) sn += cp[(size_t)q];
+    const long long num = ((long long)c % N) * (sn % N) % N;
+    const double a = kTwoPi * (double)num / N;
+    *re = std::cos(a);
+    *im = std::sin(a);
+}
+// block_phase (fc_core.cpp:41-44): exp(+j 2 pi (r c mod L) L_S mod L / L)
+void block_phase_d(long long r, int c, int L_S, int L, double* re, double* im) {
+    const long long num = r * c % L * L_S % L;
+    const double a = kTwoPi * (double)num / L;
+    *re = std::cos(a);
+    *im = std::sin(a);
+}
+float2 f2(double re, double im) { return make_float2((float)re, (float)im); }
+int check_sym(const fcw_plan* p, int m, int S) {
+    if (!p) return fail(FCW_EINVAL, "null plan");
+    if (m < 0 || m >= p->M) return fail(FCW_ERANGE, "subband index");
+    if (S < 0) return fail(FCW_EINVAL, "negative unit count");
+    return FCW_OK;
+}
+}  // namespace
+
+int fcw_symbol_phase(int n, int c, const int* cp_high, int B, int N, double* re, double* im) {
+    if (!re || !im || (n > 0 && !cp_high)) return fail(FCW_EINVAL, "null argument");
+    if (n < 0) return fail(FCW_EINVAL, "symbol index");  // fc_sync.cpp:46
+    if (n >= B && n > 0) return fail(FCW_ERANGE, "symbol index outside CP schedule");
+    if (N <= 0) return fail(FCW_EINVAL, "N must be positive");
+    std::vector<int> cp(cp_high, cp_high + (n > 0 ? B : 0));
+    symbol_phase_d(n, c, cp, N, re, im);
+    return FCW_OK;
+}
+
+int fcw_block_phase(int64_t r, int c, int L_S, int L, double* re, double* im) {
+    if (!re || !im) return fail(FCW_EINVAL, "null argument");
+    if (L <= 0) return fail(FCW_EINVAL, "L must be positive");
+    block_phase_d(r, c, L_S, L, re, im);
+    return FCW_OK;
+}
+
+int fcw_tx_symbol(const fcw_plan* p, int m, int n, const void* sym, int64_t sym_stride, int l_cp, void* out,
+                  int64_t out_stride, int S, void* stream) {
+    if (int rc = check_sym(p, m, S)) return rc;
+    if (n < 0 || n >= p->B) return fail(FCW_ERANGE, "symbol index outside CP schedule");
+    if (S == 0) return FCW_OK;
+    if (!sym || !out) return fail(FCW_EINVAL, "null buffer");
+    const auto& sb = p->subs[m];
+    if (sb.desc.l_ofdm != sb.desc.L) return fail(FCW_EINVAL, "symbol-synchronized TX requires L == L_OFDM");
+    if (l_cp < 0 || l_cp > sb.p.L_L) return fail(FCW_EINVAL, "CP exceeds leading overlap (L_CP > L_L)");  // fc_sync.cpp:35
+    if (sym_stride == 0) sym_stride = sb.desc.L + l_cp;
+    if (out_stride == 0) out_stride = 3LL * p->N / 2;
+    if (sym_stride < sb.desc.L + l_cp || out_stride < 3LL * p->N / 2) return fail(FCW_EINVAL, "stride too small");
+    double tr, ti, b1r, b1i;
+    symbol_phase_d(n, sb.desc.c, p->cp, p->N, &tr, &ti);
+    block_phase_d(1, sb.desc.c, sb.p.L_S, sb.desc.L, &b1r, &b1i);  // block_phase(0) = 1
+    const cudaError_t e = fcw::sym_tx_symbol(*p, m, static_cast<const float2*>(sym), sym_stride, l_cp, f2(tr, ti),
+                                             f2(b1r * tr - b1i * ti, b1r * ti + b1i * tr),
+                                             (float)std::sqrt((double)sb.p.I), static_cast<float2*>(out), out_stride,
+                                             S, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "tx_symbol");
+    return FCW_OK;
+}
+
+int fcw_combine_symbols(const fcw_plan* p, const void* syms, int64_t sym_unit_stride, void* wave,
+                        int64_t wave_stride, int S, void* stream) {
+    if (!p) return fail(FCW_EINVAL, "null plan");
+    if (S < 0) return fail(FCW_EINVAL, "negative unit count");
+    if (S == 0) return FCW_OK;
+    if (!syms || !wave) return fail(FCW_EINVAL, "null buffer");
+    const long long per = (long long)p->B * (3LL * p->N / 2);
+    if (sym_unit_stride == 0) sym_unit_stride = per;
+    if (wave_stride == 0) wave_stride = p->Q;
+    if (sym_unit_stride < per || wave_stride < p->Q) return fail(FCW_EINVAL, "stride too small");
+    const cudaError_t e = fcw::sym_combine(*p, static_cast<const float2*>(syms), sym_unit_stride,
+                                           static_cast<float2*>(wave), wave_stride, S,
+                                           static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "combine_symbols");
+    return FCW_OK;
+}
+
+int fcw_rx_segment(const fcw_plan* p, const void* wave, int64_t wave_stride, int64_t wave_len, int64_t useful0,
+                   int n, void* y0, void* y1, int64_t y_stride, int S, void* stream) {
+    if (!p) return fail(FCW_EINVAL, "null plan");
+    if (n < 0 || n >= p->B) return fail(FCW_ERANGE, "symbol index outside CP schedule");  // fc_sync.cpp:146-147
+    if (S < 0) return fail(FCW_EINVAL, "negative unit count");
+    const long long start = useful0 - p->pN.N_L + p->sigma[(size_t)n];
+    if (start < 0 || start + 3LL * p->N / 2 > wave_len)
+        return fail(FCW_EINVAL, "waveform too short for symbol window");  // fc_sync.cpp:149-151
+    if (S == 0) return FCW_OK;
+    if (!wave || !y0 || !y1) return fail(FCW_EINVAL, "null buffer");
+    if (wave_stride == 0) wave_stride = wave_len;
+    if (y_stride == 0) y_stride = p->N;
+    if (wave_stride < wave_len || y_stride < p->N) return fail(FCW_EINVAL, "stride too small");
+    const size_t b = sizeof(float2);
+    auto st = static_cast<cudaStream_t>(stream);
+    const float2* w = static_cast<const float2*>(wave) + start;
+    cudaError_t e = cudaMemcpy2DAsync(y0, b * y_stride, w, b * wave_stride, b * p->N, S, cudaMemcpyDeviceToDevice, st);
+    if (e == cudaSuccess)
+        e = cudaMemcpy2DAsync(y1, b * y_stride, w + p->N / 2, b * wave_stride, b * p->N, S, cudaMemcpyDeviceToDevice,
+                              st);
+    if (e != cudaSuccess) return cuda_fail(e, "rx_segment");
+    return FCW_OK;
+}
+
+int fcw_rx_block_freq(const fcw_plan* p, int m, const void* y, int64_t y_stride, double phase_re, double phase_im,
+                      void* g, int64_t g_stride, int S, void* stream) {
+    if (int rc = check_sym(p, m, S)) return rc;
+    if (S == 0) return FCW_OK;
+    if (!y || !g) return fail(FCW_EINVAL, "null buffer");
+    const int L = p->subs[m].desc.L;
+    if (y_stride == 0) y_stride = p->N;
+    if (g_stride == 0) g_stride = L;
+    if (y_stride < p->N || g_stride < L) return fail(FCW_EINVAL, "stride too small");
+    const cudaError_t e = fcw::sym_rx_block_freq(*p, m, static_cast<const float2*>(y), y_stride, f2(phase_re, -phase_im),
+                                                 static_cast<float2*>(g), g_stride, S,
+                                                 static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "rx_block_freq");
+    return FCW_OK;
+}
+
+int fcw_rx_symbol_simplified(const fcw_plan* p, int m, const void* g0, const void* g1, int64_t g_stride, void* out,
+                             int64_t out_stride, int S, void* stream) {
+    if (int rc = check_sym(p, m, S)) return rc;
+    const auto& sb = p->subs[m];
+    if (sb.p.L_S * 2 != sb.desc.L) return fail(FCW_EINVAL, "fused RX path requires 50 % overlap");  // fc_sync.cpp:199
+    if (S == 0) return FCW_OK;
+    if (!g0 || !g1 || !out) return fail(FCW_EINVAL, "null buffer");
+    const int L = sb.desc.L;
+    if (g_stride == 0) g_stride = L;
+    if (out_stride == 0) out_stride = L;
+    if (g_stride < L || out_stride < L) return fail(FCW_EINVAL, "stride too small");
+    const double scale = std::sqrt((double)sb.p.I) * ((double)L / p->N) / std::sqrt((double)L);
+    const cudaError_t e = fcw::sym_rx_simplified(*p, m, static_cast<const float2*>(g0), static_cast<const float2*>(g1),
+                                                 g_stride, (float)scale, static_cast<float2*>(out), out_stride, S,
+                                                 static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "rx_symbol_simplified");
+    return FCW_OK;
+}
+
+int fcw_rx_symbol_direct(const fcw_plan* p, int m, int n, const void* y0, const void* y1, int64_t y_stride, void* out,
+                         int64_t out_stride, int S, void* stream) {
+    if (int rc = check_sym(p, m, S)) return rc;
+    if (n < 0 || n >= p->B) return fail(FCW_ERANGE, "symbol index outside CP schedule");
+    const auto& sb = p->subs[m];
+    if (sb.desc.l_ofdm != sb.desc.L) return fail(FCW_EINVAL, "symbol-synchronized RX requires L == L_OFDM");
+    if (S == 0) return FCW_OK;
+    if (!y0 || !y1 || !out) return fail(FCW_EINVAL, "null buffer");
+    const int L = sb.desc.L;
+    if (y_stride == 0) y_stride = p->N;
+    if (out_stride == 0) out_stride = L;
+    if (y_stride < p->N || out_stride < L) return fail(FCW_EINVAL, "stride too small");
+    double tr, ti, b1r, b1i;
+    symbol_phase_d(n, sb.desc.c, p->cp, p->N, &tr, &ti);
+    block_phase_d(1, sb.desc.c, sb.p.L_S, L, &b1r, &b1i);
+    const double p1r = b1r * tr - b1i * ti, p1i = b1r * ti + b1i * tr;
+    const cudaError_t e = fcw::sym_rx_direct(*p, m, static_cast<const float2*>(y0), static_cast<const float2*>(y1),
+                                             y_stride, f2(tr, -ti), f2(p1r, -p1i), (float)std::sqrt((double)sb.p.I),
+                                             static_cast<float2*>(out), out_stride, S,
+                                             static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "rx_symbol_direct");
+    return FCW_OK;
+}
+
 int fcw_gen_qam(const fcw_plan* p, uint64_t seed, int64_t unit0, int S, int bits, void* grid, void* stream) {
     if (!p || !grid) return fail(FCW_EINVAL, "null argument");
     if (bits != 2 && bits != 4 && bits != 6 && bits != 8) return fail(FCW_EINVAL, "bits_per_symbol must be 2,4,6,8");

@@ -194,6 +194,17 @@ cudaError_t psd(const float2* wave, long long stride, long long len, int S, int 
 size_t rx_smem_bytes(const Plan& plan);
 void fill_common(const Plan& plan, KParams& kp);
 // fcw_capi.cpp: continuous FC with time-domain I/O (fcw_cont.cu)
+// reference-granularity per-symbol entry points (fcw_symbol.cu)
+cudaError_t sym_tx_symbol(const Plan& p, int m, const float2* sym, long long sym_stride, int l_cp, float2 ph0,
+                          float2 ph1, float scale, float2* out, long long out_stride, int S, cudaStream_t st);
+cudaError_t sym_combine(const Plan& p, const float2* syms, long long sym_unit_stride, float2* wave,
+                        long long wave_stride, int S, cudaStream_t st);
+cudaError_t sym_rx_block_freq(const Plan& p, int m, const float2* y, long long y_stride, float2 cph, float2* g,
+                              long long g_stride, int S, cudaStream_t st);
+cudaError_t sym_rx_simplified(const Plan& p, int m, const float2* g0, const float2* g1, long long g_stride,
+                              float scale, float2* out, long long out_stride, int S, cudaStream_t st);
+cudaError_t sym_rx_direct(const Plan& p, int m, const float2* y0, const float2* y1, long long y_stride, float2 cph0,
+                          float2 cph1, float scale, float2* out, long long out_stride, int S, cudaStream_t st);
 void plan_force_generic(fcw_plan* p);
 void plan_clear_special(fcw_plan* p);
 int tx_time_domain(const fcw_plan* p, const fc_col* td, const float2* streams, long long stream_stride,

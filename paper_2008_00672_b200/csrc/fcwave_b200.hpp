@@ -76,6 +76,28 @@ CpSplit cp_truncate(int n_cp_high, int I);
 std::int64_t symbol_sigma(int n, const CpSchedule& cps, int N);
 std::int64_t combined_length(int n_symbols, const CpSchedule& cps, const FcParams& p);
 
+// ---- reference-granularity per-symbol API (fc_sync.hpp:24-75, fc_core.hpp
+// block_phase): same signatures; each call runs one item through the per-symbol
+// device kernels of fcw_symbol.cu (host vectors in and out).
+struct FilteredSymbol {  // fc_sync.hpp:31-35
+    cvec samples;
+    int n = 0;
+};
+struct SymbolBlocks {  // fc_sync.hpp:57-59
+    cvec y0, y1;
+};
+cd symbol_phase(int n, int c, const CpSchedule& cps, int N);
+cd block_phase(std::int64_t r, int c, int L_S, int L);
+FilteredSymbol tx_symbol(const cvec& cp_ofdm_symbol, const SubbandConfig& cfg, const FcParams& p,
+                         const CpSchedule& cps, int n);
+Waveform combine_symbols(const std::vector<FilteredSymbol>& syms, const CpSchedule& cps, const FcParams& p,
+                         double fs_hz);
+SymbolBlocks rx_segment(const Waveform& w, const CpSchedule& cps, const FcParams& p, int n);
+cvec rx_symbol_direct(const cvec& y0, const cvec& y1, const SubbandConfig& cfg, const FcParams& p,
+                      const CpSchedule& cps, int n);
+cvec rx_symbol_simplified(const cvec& g0, const cvec& g1, const SubbandConfig& cfg, const FcParams& p);
+cvec rx_block_freq(const cvec& y, const SubbandConfig& cfg, const FcParams& p, cd phase);
+
 // fc_sync.hpp:52-54 — one GPU pass over all subbands.
 Waveform tx_discontinuous(const std::vector<QamGrid>& grids, const std::vector<SubbandConfig>& cfgs,
                           const CpSchedule& cps, int N, double overlap, double fs_hz);

@@ -205,3 +205,23 @@ def test_configs_import_without_product_library():
             "assert 'paper_2008_00672_b200.api' not in sys.modules; print('ok')" % ROOT)
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr
+
+
+def test_symbol_and_block_phase_match_oracle():
+    """fcw_symbol_phase / fcw_block_phase (double, host) against the oracle's
+    restatement of fc_sync.cpp:45-50 / fc_core.cpp:41-44."""
+    rng = np.random.default_rng(3)
+    cp = [352] + [288] * 13 + [352] + [288] * 5
+    cps = fb.CpSchedule(cp)
+    for _ in range(50):
+        # c >= 0: bit-exact; c < 0: the reference's truncating % gives the
+        # co-terminal angle (-x instead of 2 pi - x), equal to 1e-15
+        n, c = int(rng.integers(0, len(cp))), int(rng.integers(-5000, 5000))
+        r, L = int(rng.integers(0, 3)), int(2 ** rng.integers(2, 11))
+        a, b = fb.symbol_phase(n, c, cps, 4096), O.symbol_phase(n, c, cp, 4096)
+        e, f = fb.block_phase(r, c, L // 2, L), O.block_phase(r, c, L // 2, L)
+        if c >= 0:
+            assert a == b and e == f
+        assert abs(a - b) < 1e-15 and abs(e - f) < 1e-15
+    with pytest.raises(ValueError):
+        fb.symbol_phase(-1, 3, cps, 4096)
