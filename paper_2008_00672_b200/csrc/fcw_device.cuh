@@ -136,6 +136,9 @@ constexpr int kTw16Len = 512;            // fft256_half per-lane twiddles (unifo
 #ifndef FCW_TW16
 #define FCW_TW16 1
 #endif
+#ifndef FCW_TX_UNROLL_R
+#define FCW_TX_UNROLL_R 1  // TX half-warp pair rounds: both blocks unrolled (compile-time renames)
+#endif
 // The per-lane twiddle table follows the short and long twiddle tables in SMEM
 // (filled in the kernel prologue when P.tw16 is set).
 FCW_DI const float2* tw16_of(const KParams& P, const float2* stw) {
@@ -501,9 +504,13 @@ FCW_DI void tx_short_half(const KParams& P, const Team& tm, const SymDev& sy, co
         }
         const int lcp = sy.cp >> sd.logI;
         const int qbase = sd.c - L / 2 + t, ext0 = N + sd.ext_base;
-        const int r0 = pair ? 0 : h, r1 = pair ? 2 : h + 1;
-#pragma unroll 1
-        for (int r = r0; r < r1; ++r) {
+        // One block: its DFT inputs from x (register renames), the pruned DFT and the scatter.
+        // RC < 0: the block index is the runtime value r (tail round: r = h, lane dependent);
+        // RC = 0 / 1: compile-time block (pair rounds): plain renames, and block 1's known-zero
+        // CP positions (m < 4) join the DFT's zero mask.
+        auto block = [&](auto rc_, int r) {
+            constexpr int RC = decltype(rc_)::value;
+            if constexpr (RC >= 0) r = RC;
             // block 0: e = t + 16 m in [L/4 - lcp, 3L/4) holds x[(e - L/4) mod L] = v[(m - 4) mod 16];
             // block 1: e in [L/4, 3L/4) holds x[e + L/4] = v[m + 4]  (register renames, L/4 = 4 * 16)
             float2 u[PPT];
@@ -517,7 +524,8 @@ FCW_DI void tx_short_half(const KParams& P, const Team& tm, const SymDev& sy, co
                     u[k] = zero2();  // k >= 12: known zero (not read)
             }
             // ZV: block bins t + 16m, m in [5, 10], lie outside every window (never scattered)
-            fft256_half<-1, 0xF000ull, ZV == 1 ? (0xFFFFull & ~kZ6) : ~0ull>(u, buf, stw, t, 0, tw16_of(P, stw));
+            fft256_half<-1, RC == 1 ? 0xF00Full : 0xF000ull, ZV == 1 ? (0xFFFFull & ~kZ6) : ~0ull>(u, buf, stw, t, 0,
+                                                                                               tw16_of(P, stw));
             float2* spec = r ? spec1 : spec0;
             const float sgn = r ? sd.bp1 : 1.f;
             static_for<PPT>([&](auto kc) {
@@ -531,6 +539,14 @@ FCW_DI void tx_short_half(const KParams& P, const Team& tm, const SymDev& sy, co
                     if (act && dest >= 0) spec[dest] = cscale(u[K], __int_as_float(e.y) * sgn);
                 }
             });
+        };
+        if (FCW_TX_UNROLL_R && pair) {
+            block(IC<0>{}, 0);
+            block(IC<1>{}, 1);
+        } else {
+            const int r0 = pair ? 0 : h, r1 = pair ? 2 : h + 1;
+#pragma unroll 1
+            for (int r = r0; r < r1; ++r) block(IC<-1>{}, r);
         }
     }
 }
@@ -1059,6 +1075,10 @@ FCW_DI void rx_short_half(const KParams& P, const Team& tm, const SymDev& sy, co
     // slower here: the chain IDFT -> DFT cannot be split across halves).
     int done = 0;
     while (gcount - done > 0) {
+        // a warp with no subband left in this round leaves (warp-uniform): it
+        // goes on to the next symbol's window loads instead of transforming
+        // discarded data (23 subbands = 16 + 7: warps 4..7 skip round 2)
+        if (done + 2 * tm.warp >= gcount) break;
         const int i = done + 2 * tm.warp + h;
         done += 2 * tm.nwarp;
         const bool act = i < gcount;
@@ -1348,9 +1368,18 @@ struct RunSource {
         const int item = *s_item;
         if (item >= P.n_items) return false;
         if (gtid == 0) pending = atomicAdd(P.item_counter, 1);  // next run, in flight
-        unit = item / P.nchunks;
-        n0 = (item - unit * P.nchunks) * P.chunk;
-        n1 = min(P.B, n0 + P.chunk);
+        if (item < P.big_items) {
+            unit = item / P.nchunks;
+            n0 = (item - unit * P.nchunks) * P.chunk;
+            n1 = min(P.B, n0 + P.chunk);
+        } else {
+            // the launch's last units, in short runs (short last wave)
+            const int j = item - P.big_items;
+            const int du = j / P.nchunks2;
+            unit = P.big_units + du;
+            n0 = (j - du * P.nchunks2) * P.chunk2;
+            n1 = min(P.B, n0 + P.chunk2);
+        }
         return true;
     }
 };

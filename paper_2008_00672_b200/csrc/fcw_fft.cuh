@@ -68,22 +68,92 @@ struct Tw {
 // halves is the number of issued instructions, which bounds these kernels.
 // Per component the rounding is that of the scalar code: cmul is
 // (fma(ax, bx, -(ay by)), fma(ax, by, ay bx)) either way.
-FCW_DI float2 cadd(float2 a, float2 b) { return __fadd2_rn(a, b); }
-FCW_DI float2 csub(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+// FCW_PK_ADD / FCW_PK_MUL / FCW_PK_FMA select the packed (1) or scalar (0) form
+// of the additions, the products and the fused butterfly steps.  The integer
+// pipe shares one of the two FP32 datapaths of a sub-partition: a packed
+// instruction holds both for two cycles, so integer / move instructions never
+// overlap with it, while they pair with scalar FP32 (tools/ubench_coissue.cu).
+#ifndef FCW_PK_ADD
+#define FCW_PK_ADD 1
+#endif
+#ifndef FCW_PK_MUL
+#define FCW_PK_MUL 0
+#endif
+#ifndef FCW_PK_FMA
+#define FCW_PK_FMA 0
+#endif
+#ifndef FCW_PK_SCALE
+#define FCW_PK_SCALE FCW_PK_MUL
+#endif
+#ifndef FCW_PK_AXPY
+#define FCW_PK_AXPY FCW_PK_FMA
+#endif
+#ifndef FCW_PK_SWAP
+#define FCW_PK_SWAP FCW_PK_FMA
+#endif
+#ifndef FCW_PK_TWICE
+#define FCW_PK_TWICE FCW_PK_FMA
+#endif
+FCW_DI float2 cadd(float2 a, float2 b) {
+#if FCW_PK_ADD
+    return __fadd2_rn(a, b);
+#else
+    return make_float2(a.x + b.x, a.y + b.y);
+#endif
+}
+FCW_DI float2 csub(float2 a, float2 b) {
+#if FCW_PK_ADD
+    return __fadd2_rn(a, make_float2(-b.x, -b.y));
+#else
+    return make_float2(a.x - b.x, a.y - b.y);
+#endif
+}
 FCW_DI float2 cmul(float2 a, float2 b) {
+#if FCW_PK_MUL
     return __ffma2_rn(make_float2(a.x, a.x), b, __fmul2_rn(make_float2(a.y, a.y), make_float2(-b.y, b.x)));
+#else
+    return make_float2(fmaf(a.x, b.x, -(a.y * b.y)), fmaf(a.x, b.y, a.y * b.x));
+#endif
 }
 FCW_DI float2 cmulc(float2 a, float2 b) {  // a * conj(b)
+#if FCW_PK_MUL
     return __ffma2_rn(a, make_float2(b.x, b.x), __fmul2_rn(make_float2(a.y, a.x), make_float2(b.y, -b.y)));
+#else
+    return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -(a.x * b.y)));
+#endif
 }
-FCW_DI float2 cscale(float2 a, float s) { return __fmul2_rn(a, make_float2(s, s)); }
+FCW_DI float2 cscale(float2 a, float s) {
+#if FCW_PK_SCALE
+    return __fmul2_rn(a, make_float2(s, s));
+#else
+    return make_float2(a.x * s, a.y * s);
+#endif
+}
 FCW_DI float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
 // a + s * b (real s), one FFMA2
-FCW_DI float2 caxpy(float s, float2 b, float2 a) { return __ffma2_rn(make_float2(s, s), b, a); }
+FCW_DI float2 caxpy(float s, float2 b, float2 a) {
+#if FCW_PK_AXPY
+    return __ffma2_rn(make_float2(s, s), b, a);
+#else
+    return make_float2(fmaf(s, b.x, a.x), fmaf(s, b.y, a.y));
+#endif
+}
 // a + (p, q) * swap(b) = (a.x + p b.y, a.y + q b.x), one FFMA2: with (p, q) =
 // (-1, 1) it is a + j b, with (1, -1) a - j b
 FCW_DI float2 cswapfma(float2 b, float p, float q, float2 a) {
+#if FCW_PK_SWAP
     return __ffma2_rn(make_float2(b.y, b.x), make_float2(p, q), a);
+#else
+    return make_float2(fmaf(b.y, p, a.x), fmaf(b.x, q, a.y));
+#endif
+}
+// 2 a - y (the second output of a butterfly whose first output is y = a + w b)
+FCW_DI float2 ctwice_minus(float2 a, float2 y) {
+#if FCW_PK_TWICE
+    return __ffma2_rn(make_float2(2.f, 2.f), a, make_float2(-y.x, -y.y));
+#else
+    return make_float2(fmaf(2.f, a.x, -y.x), fmaf(2.f, a.y, -y.y));
+#endif
 }
 // multiply by j^k (compile-time k)
 template <int K>
@@ -191,7 +261,7 @@ FCW_DI void fft_stage(float2 (&x)[L]) {
                     constexpr float wi = Tw<LEN, K, SIGN>::im;
                     const float2 y0 = caxpy(wr, b, cswapfma(b, -wi, wi, a));
                     x[s + K] = y0;
-                    x[s + K + H] = __ffma2_rn(make_float2(2.f, 2.f), a, make_float2(-y0.x, -y0.y));
+                    x[s + K + H] = ctwice_minus(a, y0);
                 }
             }
             fft_stage<L, SIGN, LEN, K + 1, ZM, OM>(x);
