@@ -1368,18 +1368,9 @@ struct RunSource {
         const int item = *s_item;
         if (item >= P.n_items) return false;
         if (gtid == 0) pending = atomicAdd(P.item_counter, 1);  // next run, in flight
-        if (item < P.big_items) {
-            unit = item / P.nchunks;
-            n0 = (item - unit * P.nchunks) * P.chunk;
-            n1 = min(P.B, n0 + P.chunk);
-        } else {
-            // the launch's last units, in short runs (short last wave)
-            const int j = item - P.big_items;
-            const int du = j / P.nchunks2;
-            unit = P.big_units + du;
-            n0 = (j - du * P.nchunks2) * P.chunk2;
-            n1 = min(P.B, n0 + P.chunk2);
-        }
+        unit = item / P.nchunks;
+        n0 = (item - unit * P.nchunks) * P.chunk;
+        n1 = min(P.B, n0 + P.chunk);
         return true;
     }
 };

@@ -366,6 +366,7 @@ FCW_DI void team_pass(float2 (&v)[NF][PPT], float2* const* buf, const float2* __
     constexpr bool LAST = (NS * R == n);
     constexpr int NB = PPT / R;
     static_assert(R >= 2 && PPT % R == 0, "team_fft: bad radix schedule");
+    constexpr bool kSwz = T == 32 && (PPT == 8 || PPT == 4);  // XOR-swizzled warp layouts (saddr)
     if (act) {
 #pragma unroll
         for (int i = 0; i < NB; ++i) {
@@ -399,18 +400,29 @@ FCW_DI void team_pass(float2 (&v)[NF][PPT], float2* const* buf, const float2* __
             for (int i = 0; i < NB; ++i) {
                 const int j = t + T * i;
                 const int base = (j / NS) * NS * R + (j & (NS - 1));
+                // padded layout: with NS = 1 (base a multiple of R, R | 16) or NS a multiple of
+                // 16 the pad term of base + k NS is pad(base) + k NS / 16, so the R slots are
+                // one computed address plus compile-time offsets
+                constexpr bool kPadLinW = !kSwz && (NS == 1 || NS % 16 == 0);
+                const int wb = kPadLinW ? spad(base) : 0;
 #pragma unroll
                 for (int f = 0; f < NF; ++f)
 #pragma unroll
-                    for (int k = 0; k < R; ++k) buf[f][saddr<T, PPT>(base + k * NS)] = v[f][i + k * NB];
+                    for (int k = 0; k < R; ++k) {
+                        const int slot = kPadLinW ? wb + k * (NS + NS / 16) : saddr<T, PPT>(base + k * NS);
+                        buf[f][slot] = v[f][i + k * NB];
+                    }
             }
         }
         team_bar<CTA>(bar_id, bar_n);
         if (act) {
+            constexpr bool kPadLinR = !kSwz && T % 16 == 0;  // pad(t + T m) = pad(t) + m T / 16
+            const int rb = kPadLinR ? spad(t) : 0;
 #pragma unroll
             for (int f = 0; f < NF; ++f)
 #pragma unroll
-                for (int m = 0; m < PPT; ++m) v[f][m] = buf[f][saddr<T, PPT>(t + T * m)];
+                for (int m = 0; m < PPT; ++m)
+                    v[f][m] = buf[f][kPadLinR ? rb + m * (T + T / 16) : saddr<T, PPT>(t + T * m)];
         }
         team_pass<n, T, PPT, SIGN, NF, CTA, NS * R, TWL>(v, buf, tw, ts, t, act, bar_id, bar_n);
     }

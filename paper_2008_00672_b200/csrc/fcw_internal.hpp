@@ -55,10 +55,6 @@ struct KParams {
     int teams;           // teams per CTA (teams_per_cta<N>)
     int dynamic;         // 1: runs pulled from item_counter; 0: static balanced ranges
     int n_items, nchunks;  // dynamic mode: S * nchunks runs of `chunk` symbols
-    // dynamic TX, two run lengths: items [0, big_items) are runs of `chunk` symbols over units
-    // [0, big_units); the rest are runs of `chunk2` symbols (nchunks2 per unit) over the last
-    // units, so the launch's last wave of runs is short (big_items == n_items: one length)
-    int big_items, big_units, chunk2, nchunks2;
     int spec_stride;  // float2 per block spectrum in SMEM (>= N + n_ext, >= N + N/16)
     int scratch_stride;  // float2 per warp scratch
     int stab_len;        // entries of the SMEM short-transform twiddle table (plan Lmax)

@@ -207,33 +207,6 @@ cudaError_t launch_one(KernelFn k, size_t smem, KParams& kp, bool tx, int N, int
     // in static mode no more teams than symbols
     const long long work = kp.dynamic ? kp.n_items : (long long)kp.n_units * kp.B;
     const int grid = (int)std::max(1LL, std::min((work + G - 1) / G, (long long)per_sm * sms));
-    kp.big_items = kp.n_items;
-    kp.big_units = kp.n_units;
-    kp.chunk2 = kp.chunk;
-    kp.nchunks2 = kp.nchunks;
-    if (tx && kp.dynamic) {
-        // Long TX runs (few carry recomputes) leave a ragged last wave: the runs
-        // beyond the last full wave of resident teams, and the units they belong
-        // to, are cut into short runs instead (FCW_TAIL_CHUNK symbols, 0 = off).
-        // FCW_TAIL_UNITS forces the number of short-run units (tests).
-        const char* e = std::getenv("FCW_TAIL_CHUNK");
-        const int tail_chunk = e ? std::atoi(e) : 28;
-        int tail_units = 0;
-        if (const char* u = std::getenv("FCW_TAIL_UNITS")) {
-            tail_units = std::min(std::max(std::atoi(u), 0), kp.n_units);
-        } else if (!std::getenv("FCW_CHUNK") && !std::getenv("FCW_CHUNK_TX")) {
-            const long long teams_total = (long long)grid * G;
-            const long long full = kp.n_items / teams_total * teams_total;
-            if (full > 0 && full < kp.n_items) tail_units = kp.n_units - (int)(full / kp.nchunks);
-        }
-        if (tail_units > 0 && tail_chunk > 0 && tail_chunk < kp.chunk) {
-            kp.big_units = kp.n_units - tail_units;
-            kp.big_items = kp.big_units * kp.nchunks;
-            kp.chunk2 = tail_chunk;
-            kp.nchunks2 = (kp.B + tail_chunk - 1) / tail_chunk;
-            kp.n_items = kp.big_items + tail_units * kp.nchunks2;
-        }
-    }
     const size_t carry_bytes = tx ? (size_t)grid * G * (N / 2) * sizeof(float2) : 0;
     cudaMemPool_t pool;
     e = scratch_pool(dev, &pool);

@@ -109,23 +109,18 @@ def _hot_golden():
     return [p for p in _golden() if "packed" in np.load(p).files]
 
 
-@pytest.mark.parametrize("sched", ["default", "chunk1", "chunk7", "static", "twolevel"])
+@pytest.mark.parametrize("sched", ["default", "chunk1", "chunk7", "static"])
 @pytest.mark.parametrize("path", _hot_golden(), ids=lambda p: os.path.basename(p)[:-4])
 def test_gpu_matches_reference_golden_hot_geometry(path, sched, monkeypatch):
     """The UNMODIFIED reference's outputs at the exact geometry of BASELINE
     configs 5 (g7: 23 x L=256, the zero-bin kernel variant) and 4 (g8: 273 x
     L=16), through the same packed-grid plan and kernels bench.py times, under
     every work schedule (chunk1 / chunk7: a TX carry recompute at every run
-    start; twolevel: the full-load TX schedule's two run lengths, long runs on
-    the first unit and short runs on the last two)."""
+    start)."""
     if sched.startswith("chunk"):
         monkeypatch.setenv("FCW_CHUNK", sched[5:])
     elif sched == "static":
         monkeypatch.setenv("FCW_SCHED", "static")
-    elif sched == "twolevel":
-        monkeypatch.setenv("FCW_CHUNK_TX", "6")
-        monkeypatch.setenv("FCW_TAIL_UNITS", "2")
-        monkeypatch.setenv("FCW_TAIL_CHUNK", "4")
     z = np.load(path)
     N, cp = int(z["N"]), z["cp"].tolist()
     Ls, cs = z["Ls"].tolist(), z["cs"].tolist()
