@@ -407,6 +407,13 @@ int fcw_plan_create(fcw_plan** out, int N, double overlap, const int* cp_high, i
             if ((float)s.window[b ^ 128] != 0.0f) p->zv = false;
             if (p->h_inv[(size_t)m * 256 + b] >= 0) p->zv = false;
         }
+        // ... and its active map is the centred one (centered_active_map without a DC
+        // gap): active index a sits on DFT bin (a - n_act/2) mod L, so the kernels
+        // compute the packed-row index of bin b as (b + n_act/2) mod L without a table
+        for (int b = 0; b < 256 && p->zv; ++b) {
+            const int a = (b + s.n_active / 2) & 255;
+            if (p->h_inv[(size_t)m * 256 + b] != (a < s.n_active ? a : -1)) p->zv = false;
+        }
     }
     // secondary contributions: ext slots numbered subband-major (a subband's
     // secondary bins are consecutive from its ext_base); the fix-up list is

@@ -478,8 +478,15 @@ FCW_DI void tx_short_half(const KParams& P, const Team& tm, const SymDev& sy, co
             auto live = [&](int k) { return !((ZI >> k) & 1ull); };
             int inv[PPT];
 #pragma unroll
-            for (int k = 0; k < PPT; ++k)
-                inv[k] = (act && live(k)) ? (int)(short)(__ldg(&ce[TW * k]).x & 0xffff) : -1;
+            for (int k = 0; k < PPT; ++k) {
+                if constexpr (ZV == 1) {
+                    // zv plans have centred active maps: no table load ahead of the gather
+                    const int a = (t + TW * k + (sd.n_act >> 1)) & (L - 1);
+                    inv[k] = (act && live(k) && a < sd.n_act) ? a : -1;
+                } else {
+                    inv[k] = (act && live(k)) ? (int)(short)(__ldg(&ce[TW * k]).x & 0xffff) : -1;
+                }
+            }
             if (P.grid_full) {
                 const float2* g = row + sd.full_off + t;
 #pragma unroll
@@ -1122,8 +1129,15 @@ FCW_DI void rx_short_half(const KParams& P, const Team& tm, const SymDev& sy, co
                 constexpr unsigned long long ZO = ZV == 1 ? kZ6 : 0ull;  // ZV: inactive bins, nothing to store
                 int inv[PPT];  // all entry loads in flight before the first store
 #pragma unroll
-                for (int k = 0; k < PPT; ++k)
-                    inv[k] = ((ZO >> k) & 1ull) ? -1 : (int)(short)(__ldg(&ce[TW * k]).x & 0xffff);
+                for (int k = 0; k < PPT; ++k) {
+                    if constexpr (ZV == 1) {
+                        // zv plans have centred active maps (see tx_short_half)
+                        const int a = (t + TW * k + (sd.n_act >> 1)) & (L - 1);
+                        inv[k] = (!((ZO >> k) & 1ull) && a < sd.n_act) ? a : -1;
+                    } else {
+                        inv[k] = ((ZO >> k) & 1ull) ? -1 : (int)(short)(__ldg(&ce[TW * k]).x & 0xffff);
+                    }
+                }
 #pragma unroll
                 for (int k = 0; k < PPT; ++k)
                     if (!((ZO >> k) & 1ull) && inv[k] >= 0) {
