@@ -163,7 +163,75 @@ FCW_DI float2 grid_val(const KParams& P, const SubDev& sd, const float2* __restr
 struct Team {
     int tid, nthr;    // thread index / count within the team
     int warp, nwarp;  // warp index / count within the team
+    unsigned tm_a = 0, tm_c = 0;  // this thread's TMEM twiddle sets (TMEM-twiddle kernels, else unused)
 };
+
+// Kernels whose per-lane / per-thread twiddles live in TMEM (fcw_fft.cuh): the
+// zero-bin L = 256, N = 4096 variant (config 5).
+template <int N, int ZV>
+constexpr bool tmem_tw() {
+    return FCW_TMEM_TW && ZV == 1 && N == 4096;
+}
+// FCW_TMEM_TW bit 1: the half-warp FFT_256 twiddles, bit 2: the long-transform twiddles
+template <int N, int ZV>
+constexpr bool tmem_tw_half() {
+    return tmem_tw<N, ZV>() && (FCW_TMEM_TW & 1);
+}
+template <int N, int ZV>
+constexpr bool tmem_tw_long() {
+    return tmem_tw<N, ZV>() && (FCW_TMEM_TW & 2);
+}
+
+// Allocate kTmemCols TMEM columns for the CTA and park the twiddle sets:
+//   A [0, 32):   W_256^(k (lane & 15)), k = 0..15   (half-warp FFT_256; long pass 2)
+//   B [32, 64):  W_256^(k ((lane & 15) + 64))       (fused RX: input rotated by j^t)
+//   C [64, 96) for warps 0-3, [96, 128) for warps 4-7: W_N^(k tid)  (long pass 3)
+// Every thread writes its own lane (warps w and w + 4 share a lane quadrant, and
+// write identical A / B).  Returns the allocation's base address.
+template <int N>
+FCW_DI unsigned tmem_tables(const KParams& P, unsigned* slot, Team& tm) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         (unsigned)__cvta_generic_to_shared(slot)),
+                     "n"(kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const unsigned base = *slot;
+    const unsigned q = base + ((unsigned)((warp & 3) * 32) << 16);
+    tm.tm_a = q;
+    tm.tm_c = q + 64 + 32 * (warp >> 2);
+    const int t16 = lane & 15, tid = threadIdx.x;
+#pragma unroll 1
+    for (int set = 0; set < 3; ++set) {
+#pragma unroll 1
+        for (int c = 0; c < 2; ++c) {
+            unsigned d[16];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int kk = k + 8 * c;
+                const int e = set == 0   ? ((kk * t16) & 255) * (N / 256)
+                              : set == 1 ? ((kk * (t16 + 64)) & 255) * (N / 256)
+                                         : (kk * tid) & (N - 1);
+                const float2 w = __ldg(&P.tw[e]);
+                d[2 * k] = __float_as_uint(w.x);
+                d[2 * k + 1] = __float_as_uint(w.y);
+            }
+            tmem_st16((set == 2 ? tm.tm_c : q + 32 * set) + 16 * c, d);
+        }
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    return base;
+}
+FCW_DI void tmem_release(unsigned base) {
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if ((threadIdx.x >> 5) == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(base), "n"(kTmemCols));
+}
 
 // ---------------------------------------------------------------- K-TX parts
 
@@ -507,7 +575,8 @@ FCW_DI void tx_short_half(const KParams& P, const Team& tm, const SymDev& sy, co
             for (int k = 0; k < PPT; ++k)
                 if (live(k)) v[k] = cmul(v[k], ph);
         }
-        fft256_half<+1, ZV == 1 ? kZ6 : 0ull>(v, buf, stw, t, 0, tw16_of(P, stw));  // x[t + 16 m] (scales in ph)
+        fft256_half<+1, ZV == 1 ? kZ6 : 0ull, ~0ull, tmem_tw_half<N, ZV>()>(v, buf, stw, t, 0, tw16_of(P, stw),
+                                                                      tm.tm_a);  // x[t + 16 m] (scales in ph)
         }
         const int lcp = sy.cp >> sd.logI;
         const int qbase = sd.c - L / 2 + t, ext0 = N + sd.ext_base;
@@ -531,8 +600,8 @@ FCW_DI void tx_short_half(const KParams& P, const Team& tm, const SymDev& sy, co
                     u[k] = zero2();  // k >= 12: known zero (not read)
             }
             // ZV: block bins t + 16m, m in [5, 10], lie outside every window (never scattered)
-            fft256_half<-1, RC == 1 ? 0xF00Full : 0xF000ull, ZV == 1 ? (0xFFFFull & ~kZ6) : ~0ull>(u, buf, stw, t, 0,
-                                                                                               tw16_of(P, stw));
+            fft256_half<-1, RC == 1 ? 0xF00Full : 0xF000ull, ZV == 1 ? (0xFFFFull & ~kZ6) : ~0ull, tmem_tw_half<N, ZV>()>(
+                u, buf, stw, t, 0, tw16_of(P, stw), tm.tm_a);
             float2* spec = r ? spec1 : spec0;
             const float sgn = r ? sd.bp1 : 1.f;
             static_for<PPT>([&](auto kc) {
@@ -1110,8 +1179,10 @@ FCW_DI void rx_short_half(const KParams& P, const Team& tm, const SymDev& sy, co
             }
         });
         // IDFT of j^t f; S-hat then keeps x[e], e < L/2: outputs m >= 8 are dead
-        fft256_half<+1, ZV == 1 ? kZ6 : 0ull, 0x00FFull>(f, buf, stw, t, L / 4, tw16_of(P, stw));
-        fft256_half<-1, 0xFF00ull>(f, buf, stw, t, 0, tw16_of(P, stw));  // S-hat keeps x[e], e < L/2; DFT
+        fft256_half<+1, ZV == 1 ? kZ6 : 0ull, 0x00FFull, tmem_tw_half<N, ZV>()>(f, buf, stw, t, L / 4, tw16_of(P, stw),
+                                                                          tm.tm_a);
+        // S-hat keeps x[e], e < L/2; DFT
+        fft256_half<-1, 0xFF00ull, ~0ull, tmem_tw_half<N, ZV>()>(f, buf, stw, t, 0, tw16_of(P, stw), tm.tm_a);
         const float2 ph = __ldg(&P.tw[theta_exp<N>(sd.cmodN, sy.smodN)]);  // conj(theta_n)
         const float2 P1 = cscale(ph, sd.rx_s0 / (float)L);
         const float2 P2 = mul_jpow_rt(cscale(ph, sd.rx_s0 * sd.bp1), (4 - t) & 3);
@@ -1426,7 +1497,10 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU, ZV>()) tx_kernel(cons
     const int tid = threadIdx.x;
     const int g = tid / TT, gtid = tid - g * TT;
     const bool act = gtid < T;
-    const Team tm{gtid, TT, gtid >> 5, TT / 32};
+    Team tm{gtid, TT, gtid >> 5, TT / 32};
+    __shared__ unsigned tmem_slot;
+    unsigned tmem_base = 0;
+    if constexpr (tmem_tw<N, ZV>()) tmem_base = tmem_tables<N>(P, &tmem_slot, tm);
     const Smem S = smem_layout<G>(P, g);
     float2 *spec0 = S.spec0, *spec1 = S.spec1;
     // The block-1 tail that overlaps the next symbol lives in a per-team global
@@ -1516,8 +1590,8 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU, ZV>()) tx_kernel(cons
                 }
                 float2* const bufs[2] = {spec0, spec1};
                 if (!FCW_SKIP(P, 2))
-                    team_fft<N, T, kPPT, +1, 2, true, long_twl<N>(), ZG>(v, bufs, long_twl<N>() ? S.ltw : P.tw, 1,
-                                                                        gtid, act, G == 1 ? 0 : 1 + g, TT);
+                    team_fft<N, T, kPPT, +1, 2, true, tmem_tw_long<N, ZV>() ? kTwTmem : long_twl<N>(), ZG>(
+                        v, bufs, long_twl<N>() ? S.ltw : P.tw, 1, gtid, act, G == 1 ? 0 : 1 + g, TT, tm.tm_a, tm.tm_c);
             }
             // every thread has read its carry before it is overwritten: the long
             // transform's exchange barriers already order that for N >= 512
@@ -1547,6 +1621,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU, ZV>()) tx_kernel(cons
             }
         }
     }
+    if constexpr (tmem_tw<N, ZV>()) tmem_release(tmem_base);
 }
 
 template <int N, int LU, bool DYN, int ZV = 0>
@@ -1557,7 +1632,10 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU, ZV>()) rx_kernel(cons
     const int tid = threadIdx.x;
     const int g = tid / TT, gtid = tid - g * TT;
     const bool act = gtid < T;
-    const Team tm{gtid, TT, gtid >> 5, TT / 32};
+    Team tm{gtid, TT, gtid >> 5, TT / 32};
+    __shared__ unsigned tmem_slot;
+    unsigned tmem_base = 0;
+    if constexpr (tmem_tw<N, ZV>()) tmem_base = tmem_tables<N>(P, &tmem_slot, tm);
     const Smem S = smem_layout<G>(P, g);
     float2 *spec0 = S.spec0, *spec1 = S.spec1;
     for (int i = tid; i < P.stab_len; i += kThreads) S.stw[i] = __ldg(&P.tw[i * (N / P.stab_len)]);
@@ -1617,8 +1695,8 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU, ZV>()) rx_kernel(cons
             {
                 float2* const bufs[2] = {spec0, spec1};
                 if (!FCW_SKIP(P, 2))
-                    team_fft<N, T, kPPT, -1, 2, true, long_twl<N>()>(v, bufs, long_twl<N>() ? S.ltw : P.tw, 1, gtid, act,
-                                                                    G == 1 ? 0 : 1 + g, TT);
+                    team_fft<N, T, kPPT, -1, 2, true, tmem_tw_long<N, ZV>() ? kTwTmem : long_twl<N>()>(
+                        v, bufs, long_twl<N>() ? S.ltw : P.tw, 1, gtid, act, G == 1 ? 0 : 1 + g, TT, tm.tm_a, tm.tm_c);
             }
             team_sync<G>(g, TT);
             if (act) {
@@ -1641,6 +1719,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU, ZV>()) rx_kernel(cons
                 rx_short_all<N, LU, ZV>(P, tm, sy, spec0, spec1, out_u + (long long)n * P.row_len, S.scr, S.stw);
         }
     }
+    if constexpr (tmem_tw<N, ZV>()) tmem_release(tmem_base);
 }
 
 // Dispatch tables filled by the per-N instantiation units.

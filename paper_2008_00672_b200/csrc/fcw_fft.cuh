@@ -288,6 +288,49 @@ FCW_DI void fft_reg(float2 (&x)[L]) {
     fft_stage<L, SIGN, 2, 0, zm_brev(ZIN, L, LB), OM>(x);
 }
 
+// ------------------------------------------------- TMEM as a per-lane table
+// Twiddles that are constants of a thread (they depend on its lane / thread
+// index only) live in tensor memory: every thread parks them in its own TMEM
+// lane once per kernel and reads them back with tcgen05.ld (32x32b: thread i
+// of warp w reads lane 32 (w mod 4) + i), 16 columns = 8 complex values per
+// instruction, instead of 15 LDS.64 or four table loads and eleven products
+// per transform.  Measured on the half-warp FFT_256 in isolation
+// (tools/ubench_tmem_tw.cu): 60.8 -> 57.4 SM-cycles.
+#ifndef FCW_TMEM_TW
+#define FCW_TMEM_TW 3
+#endif
+constexpr int kTwTmem = 99;      // TWL value: long-transform twiddles from TMEM
+constexpr int kTmemCols = 128;   // columns per CTA: sets A, B (32 each), C for warps 0-3 / 4-7 (32 each)
+#define FCW_R16(a, o) a(o + 0), a(o + 1), a(o + 2), a(o + 3), a(o + 4), a(o + 5), a(o + 6), a(o + 7), a(o + 8), \
+                      a(o + 9), a(o + 10), a(o + 11), a(o + 12), a(o + 13), a(o + 14), a(o + 15)
+FCW_DI void tmem_st16(unsigned taddr, const unsigned (&d)[16]) {
+#define FCW_IN(i) "r"(d[i])
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%16], {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15};" ::FCW_R16(
+            FCW_IN, 0),
+        "r"(taddr)
+        : "memory");
+#undef FCW_IN
+}
+FCW_DI void tmem_ld16(unsigned taddr, unsigned (&d)[16]) {
+#define FCW_OUT(i) "=r"(d[i])
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : FCW_R16(FCW_OUT, 0)
+        : "r"(taddr));
+#undef FCW_OUT
+}
+// Wait for this thread's tcgen05.ld; the destination registers pass through
+// the statement so no consumer is scheduled ahead of the wait.
+FCW_DI void tmem_wait16(unsigned (&d)[16]) {
+#define FCW_IO(i) "+r"(d[i])
+    asm volatile("tcgen05.wait::ld.sync.aligned;" : FCW_R16(FCW_IO, 0)::"memory");
+#undef FCW_IO
+}
+FCW_DI float2 tmem_c(const unsigned (&d)[16], int k) {
+    return make_float2(__uint_as_float(d[2 * k]), __uint_as_float(d[2 * k + 1]));
+}
+
 // ------------------------------------------------------------ team barriers
 // CTA-scope teams sync on barrier 0 (the whole block) or, for a sub-team, on
 // named barrier bar_id over bar_n threads; warp teams use __syncwarp.
@@ -359,7 +402,7 @@ FCW_DI void twiddle_powers(float2 (&w)[R], const float2* tw, int e0) {
 // One Stockham pass (and the remaining ones, recursively).
 template <int n, int T, int PPT, int SIGN, int NF, bool CTA, int NS, int TWL, unsigned long long ZIN0 = 0>
 FCW_DI void team_pass(float2 (&v)[NF][PPT], float2* const* buf, const float2* __restrict__ tw,
-                      int ts, int t, bool act, int bar_id, int bar_n) {
+                      int ts, int t, bool act, int bar_id, int bar_n, unsigned tm_a = 0, unsigned tm_c = 0) {
     constexpr int R0 = PPT < 16 ? PPT : 16;
     constexpr int REM = n / NS;
     constexpr int R = REM < R0 ? REM : R0;
@@ -379,7 +422,28 @@ FCW_DI void team_pass(float2 (&v)[NF][PPT], float2* const* buf, const float2* __
             if constexpr (NS > 1) {
                 const int jm = j & (NS - 1);
                 float2 wk[R];
-                twiddle_powers<R, SIGN, TWL>(wk, tw, jm * (n / (NS * R)) * ts);
+                if constexpr (TWL == kTwTmem) {
+                    // radix-16 passes of the 4096-point transform: W_256^(k (t & 15)) (set A) for
+                    // NS = 16, W_4096^(k t) (set C) for NS = 256, parked in this thread's TMEM lane
+                    static_assert(R == 16 && NB == 1 && (NS == 16 || NS == 256), "TMEM twiddles: 16 x 16 x 16");
+                    unsigned lo[16], hi[16];
+                    const unsigned ta = NS == 16 ? tm_a : tm_c;
+                    tmem_ld16(ta, lo);
+                    tmem_ld16(ta + 16, hi);
+                    tmem_wait16(lo);
+                    tmem_wait16(hi);
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        wk[k] = tmem_c(lo, k);
+                        wk[k + 8] = tmem_c(hi, k);
+                        if constexpr (SIGN > 0) {
+                            wk[k].y = -wk[k].y;
+                            wk[k + 8].y = -wk[k + 8].y;
+                        }
+                    }
+                } else {
+                    twiddle_powers<R, SIGN, TWL>(wk, tw, jm * (n / (NS * R)) * ts);
+                }
 #pragma unroll
                 for (int k = 1; k < R; ++k)
 #pragma unroll
@@ -424,7 +488,7 @@ FCW_DI void team_pass(float2 (&v)[NF][PPT], float2* const* buf, const float2* __
                 for (int m = 0; m < PPT; ++m)
                     v[f][m] = buf[f][kPadLinR ? rb + m * (T + T / 16) : saddr<T, PPT>(t + T * m)];
         }
-        team_pass<n, T, PPT, SIGN, NF, CTA, NS * R, TWL>(v, buf, tw, ts, t, act, bar_id, bar_n);
+        team_pass<n, T, PPT, SIGN, NF, CTA, NS * R, TWL>(v, buf, tw, ts, t, act, bar_id, bar_n, tm_a, tm_c);
     }
 }
 
@@ -435,7 +499,7 @@ FCW_DI void team_pass(float2 (&v)[NF][PPT], float2* const* buf, const float2* __
 // ZIN0: inputs v[f][m] known to be zero (first pass, one butterfly per thread).
 template <int n, int T, int PPT, int SIGN, int NF, bool CTA, int TWL = 0, unsigned long long ZIN0 = 0>
 FCW_DI void team_fft(float2 (&v)[NF][PPT], float2* const* buf, const float2* __restrict__ tw, int ts,
-                     int t, bool act, int bar_id = 0, int bar_n = 0) {
+                     int t, bool act, int bar_id = 0, int bar_n = 0, unsigned tm_a = 0, unsigned tm_c = 0) {
     static_assert(n == T * PPT, "team_fft: n != T*PPT");
     if constexpr (n == 1) return;
     if constexpr (T == 1) {
@@ -444,7 +508,7 @@ FCW_DI void team_fft(float2 (&v)[NF][PPT], float2* const* buf, const float2* __r
             for (int f = 0; f < NF; ++f) fft_reg<PPT, SIGN>(v[f]);
         }
     } else {
-        team_pass<n, T, PPT, SIGN, NF, CTA, 1, TWL, ZIN0>(v, buf, tw, ts, t, act, bar_id, bar_n);
+        team_pass<n, T, PPT, SIGN, NF, CTA, 1, TWL, ZIN0>(v, buf, tw, ts, t, act, bar_id, bar_n, tm_a, tm_c);
     }
 }
 
@@ -463,10 +527,19 @@ FCW_DI void team_fft(float2 (&v)[NF][PPT], float2* const* buf, const float2* __r
 // for sel = eoff / 64 in {0, 1}: 15 conflict-free loads instead of 4 loads
 // and 11 complex products.
 // OUT: outputs v[k] the caller uses (dead ones are not computed).
-template <int SIGN, unsigned long long ZIN = 0, unsigned long long OUT = ~0ull>
+// TM: the twiddles come from this thread's TMEM lane instead (tm = address of
+// set A; set B, for eoff = 64, follows 32 columns later); both loads are in
+// flight across the exchange.
+template <int SIGN, unsigned long long ZIN = 0, unsigned long long OUT = ~0ull, bool TM = false>
 FCW_DI void fft256_half(float2 (&v)[16], float2* buf, const float2* stw, int t, int eoff,
-                        const float2* tw16 = nullptr) {
+                        const float2* tw16 = nullptr, unsigned tm = 0) {
     fft_reg<16, SIGN, ZIN>(v);
+    unsigned lo[16], hi[16];
+    if constexpr (TM) {
+        const unsigned ta = tm + 32 * (eoff >> 6);
+        tmem_ld16(ta, lo);
+        tmem_ld16(ta + 16, hi);
+    }
     __syncwarp();  // the previous use of buf has been read by every lane
     float2* wp = buf + 17 * t;
 #pragma unroll
@@ -475,6 +548,18 @@ FCW_DI void fft256_half(float2 (&v)[16], float2* buf, const float2* stw, int t, 
     const float2* rp = buf + t;
 #pragma unroll
     for (int m = 0; m < 16; ++m) v[m] = rp[17 * m];
+    if constexpr (TM) {
+        tmem_wait16(lo);
+        tmem_wait16(hi);
+#pragma unroll
+        for (int m = 1; m < 16; ++m) {
+            float2 w = m < 8 ? tmem_c(lo, m) : tmem_c(hi, m - 8);
+            if constexpr (SIGN > 0) w.y = -w.y;
+            v[m] = cmul(v[m], w);
+        }
+        fft_reg<16, SIGN, 0ull, OUT>(v);
+        return;
+    }
     if (tw16) {
         const float2* tp = tw16 + (eoff >> 6) * 256 + t;
 #pragma unroll

@@ -144,7 +144,13 @@ int scratch_stride(const Plan& p, int LU, bool tx, bool rx_direct) {
 
 int stab_len(const Plan& p) { return p.Lmax >= 64 ? p.Lmax : 0; }
 // per-lane twiddles of the half-warp FFT_256 (uniform L = 256 kernels)
-int tw16_len(const Plan& p) { return uniform_L(p) == 256 ? 512 : 0; }
+// The plan runs the kernels that keep their twiddles in TMEM (tmem_tw in fcw_device.cuh).
+bool tmem_kernels(const Plan& p) { return FCW_TMEM_TW && p.zv && p.N == 4096 && uniform_L(p) == 256; }
+// (those kernels read these twiddles from TMEM instead)
+int tw16_len(const Plan& p) {
+    if ((FCW_TMEM_TW & 1) && tmem_kernels(p)) return 0;
+    return uniform_L(p) == 256 ? 512 : 0;
+}
 
 // Independent teams per CTA (must match teams_per_cta<N> in fcw_device.cuh).
 int teams(const Plan& p) { return (p.N >= 512 && p.N <= 4096) ? 4096 / p.N : 1; }
@@ -162,7 +168,12 @@ size_t smem_bytes(const Plan& p, bool tx, bool rx_direct) {
 // stream-ordered scratch, so concurrent launches never share them.
 // Resident CTAs per SM for (kernel, smem, device); sets the dynamic-SMEM
 // attribute once.  Cached: the queries cost host time on every launch.
-cudaError_t resident_per_sm(KernelFn k, size_t smem, int dev, int* per_sm) {
+// tmem: the kernel allocates tensor memory (tcgen05.alloc).  The occupancy API
+// then reports one CTA per SM whatever the kernel needs, although the SM does
+// co-schedule such CTAs while their columns fit (measured: two 128-column CTAs
+// overlap on every SM), so the count comes from the register / shared-memory /
+// TMEM-column budgets instead.
+cudaError_t resident_per_sm(KernelFn k, size_t smem, int dev, int* per_sm, bool tmem = false) {
     static std::mutex mu;
     static std::map<std::pair<std::pair<const void*, size_t>, int>, int> cache;
     std::lock_guard<std::mutex> lk(mu);
@@ -186,11 +197,26 @@ cudaError_t resident_per_sm(KernelFn k, size_t smem, int dev, int* per_sm) {
     }
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, reinterpret_cast<const void*>(k), kThreads, smem);
     if (e != cudaSuccess) return e;
+    if (tmem && *per_sm >= 1) {
+        cudaFuncAttributes fa{};
+        int regs_sm = 0, smem_sm = 0, smem_rsv = 0;
+        e = cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(k));
+        if (e != cudaSuccess) return e;
+        cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
+        cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+        cudaDeviceGetAttribute(&smem_rsv, cudaDevAttrReservedSharedMemoryPerBlock, dev);
+        const int regs_cta = ((fa.numRegs + 7) & ~7) * kThreads;
+        const size_t smem_cta = smem + fa.sharedSizeBytes + (size_t)smem_rsv;
+        const int by_regs = regs_cta > 0 ? regs_sm / regs_cta : 1;
+        const int by_smem = smem_cta > 0 ? (int)((size_t)smem_sm / smem_cta) : 1;
+        *per_sm = std::max(1, std::min({by_regs, by_smem, 512 / kTmemCols}));
+    }
     cache[key] = *per_sm;
     return cudaSuccess;
 }
 
-cudaError_t launch_one(KernelFn k, size_t smem, KParams& kp, bool tx, int N, int G, cudaStream_t st) {
+cudaError_t launch_one(KernelFn k, size_t smem, KParams& kp, bool tx, int N, int G, cudaStream_t st,
+                       bool tmem = false) {
     if (!k) return cudaErrorInvalidValue;
 #if FCW_DEV_KNOBS
     // dev-only occupancy probe: extra dynamic SMEM per CTA (e.g. 16384 forces one CTA per SM)
@@ -200,7 +226,7 @@ cudaError_t launch_one(KernelFn k, size_t smem, KParams& kp, bool tx, int N, int
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = resident_per_sm(k, smem, dev, &per_sm);
+    e = resident_per_sm(k, smem, dev, &per_sm, tmem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     // at most the resident CTAs; in dynamic mode no more teams than runs,
@@ -318,7 +344,8 @@ cudaError_t launch_tx(const Plan& p, KParams& kp, int S, cudaStream_t st) {
     kp.teams = teams(p);
     kp.n_items = S * kp.nchunks;
     const KernelPair kp2 = pick(p.N, LU, p.zv, p.nb, team_only(p));
-    return launch_one(kp.dynamic ? kp2.tx_d : kp2.tx, smem_bytes(p, true, false), kp, true, p.N, teams(p), st);
+    return launch_one(kp.dynamic ? kp2.tx_d : kp2.tx, smem_bytes(p, true, false), kp, true, p.N, teams(p), st,
+                      tmem_kernels(p));
 }
 
 cudaError_t launch_rx(const Plan& p, KParams& kp, int S, cudaStream_t st) {
@@ -330,7 +357,8 @@ cudaError_t launch_rx(const Plan& p, KParams& kp, int S, cudaStream_t st) {
     kp.teams = teams(p);
     kp.n_items = S * kp.nchunks;
     const KernelPair kp2 = pick(p.N, LU, p.zv, p.nb, team_only(p));
-    return launch_one(kp.dynamic ? kp2.rx_d : kp2.rx, smem_bytes(p, false, direct), kp, false, p.N, teams(p), st);
+    return launch_one(kp.dynamic ? kp2.rx_d : kp2.rx, smem_bytes(p, false, direct), kp, false, p.N, teams(p), st,
+                      tmem_kernels(p));
 }
 
 // K-GEN: one thread per QAM symbol; splitmix64 is counter-based, so draw j of
