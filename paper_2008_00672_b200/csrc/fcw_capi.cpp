@@ -547,6 +547,51 @@ int fcw_plan_create(fcw_plan** out, int N, double overlap, const int* cp_high, i
             }
             d.cls_off = it->second;
         }
+        // The zv kernels keep per-lane (weight, slot code) rows of the classes in TMEM
+        // (tmem_tables in fcw_device.cuh).  Both half-warps of a warp read their row with one
+        // tcgen05.ld, so a row holds a PAIR of classes: the classes of the two subbands the fixed
+        // schedule puts side by side in one warp (TX: pair rounds (done + 2w, done + 2w + 1) while
+        // more than one subband per warp remains, then one subband per warp; RX: pair rounds
+        // throughout; a missing partner repeats the last subband).  At most kMaxTmemClasses rows.
+        if (p->zv) {
+            const int W = fcw::kWarps;
+            std::vector<std::pair<int, int>> rows;
+            auto cls = [&](int m) { return p->h_sub[std::min(m, M - 1)].cls_off / 256; };
+            auto row_of = [&](int a, int b) {
+                const std::pair<int, int> key(cls(a), cls(b));
+                for (size_t j = 0; j < rows.size(); ++j)
+                    if (rows[j] == key) return (int)j;
+                rows.push_back(key);
+                return (int)rows.size() - 1;
+            };
+            for (int done = 0; done < M;) {  // TX (tx_short_half)
+                const bool pair = M - done > W;
+                for (int w = 0; w < W; ++w) {
+                    const int a = pair ? done + 2 * w : done + w, b = pair ? a + 1 : a;
+                    if (a >= M) break;
+                    const int j = row_of(a, b);
+                    p->h_sub[a].row_tx = j;
+                    if (b < M) p->h_sub[b].row_tx = j;
+                }
+                done += pair ? 2 * W : W;
+            }
+            for (int done = 0; done < M; done += 2 * W)  // RX (rx_short_half)
+                for (int w = 0; w < W; ++w) {
+                    const int a = done + 2 * w, b = a + 1;
+                    if (a >= M) break;
+                    const int j = row_of(a, b);
+                    p->h_sub[a].row_rx = j;
+                    if (b < M) p->h_sub[b].row_rx = j;
+                }
+            if ((int)rows.size() > fcw::kMaxTmemClasses) {
+                p->zv = false;
+            } else {
+                for (const auto& r : rows) {
+                    p->h_combo.push_back(r.first);
+                    p->h_combo.push_back(r.second);
+                }
+            }
+        }
     }
     // device tables in one blob
     std::vector<float2> tw(N);

@@ -164,6 +164,7 @@ struct Team {
     int tid, nthr;    // thread index / count within the team
     int warp, nwarp;  // warp index / count within the team
     unsigned tm_a = 0, tm_c = 0;  // this thread's TMEM twiddle sets (TMEM-twiddle kernels, else unused)
+    unsigned tm_k = 0;            // ... and its bin-class rows (32 columns per class)
 };
 
 // Kernels whose per-lane / per-thread twiddles live in TMEM (fcw_fft.cuh): the
@@ -186,8 +187,15 @@ constexpr bool tmem_tw_long() {
 //   A [0, 32):   W_256^(k (lane & 15)), k = 0..15   (half-warp FFT_256; long pass 2)
 //   B [32, 64):  W_256^(k ((lane & 15) + 64))       (fused RX: input rotated by j^t)
 //   C [64, 96) for warps 0-3, [96, 128) for warps 4-7: W_N^(k tid)  (long pass 3)
+//   K [128 + 32 j, + 32), row j < P.n_combo: the bin-class row of class P.combo[j][h] for the
+//     threads of half-warp h (the two subbands a warp transforms side by side may differ in
+//     class, and the warp reads its row with one tcgen05.ld), for the lane t = lane & 15 — 16 window weights w[t + 16 k] (columns 0-15) and 16 slot codes
+//     (columns 16-31) of the bin's shifted position p0 = b ^ 128: rel = p0 - 128 for a primary
+//     bin (spectrum slot (c_m + rel) mod N), kCodeExt + s for the subband's s-th secondary bin
+//     (extension slot), kCodeNone for a zero-weight bin (tx_short_half scatter, rx_short_half).
 // Every thread writes its own lane (warps w and w + 4 share a lane quadrant, and
-// write identical A / B).  Returns the allocation's base address.
+// write identical A / B / K).  Returns the allocation's base address.
+constexpr int kCodeExt = 0x1000, kCodeNone = 0x4000;  // slot codes of the TMEM bin-class rows
 template <int N>
 FCW_DI unsigned tmem_tables(const KParams& P, unsigned* slot, Team& tm) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -222,6 +230,21 @@ FCW_DI unsigned tmem_tables(const KParams& P, unsigned* slot, Team& tm) {
             }
             tmem_st16((set == 2 ? tm.tm_c : q + 32 * set) + 16 * c, d);
         }
+    }
+    tm.tm_k = q + 128;
+    for (int j = 0; j < P.n_combo && j < kMaxTmemClasses; ++j) {
+        const int c = P.combo[j][lane >> 4];
+        unsigned wv[16], cv[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            const int b = t16 + 16 * k;
+            const int2 e = __ldg(&P.cls[c * 256 + b]);
+            const int sec = e.x >> 16;
+            wv[k] = (unsigned)e.y;
+            cv[k] = (unsigned)(sec >= 0 ? kCodeExt + sec : (sec == -1 ? (b ^ 128) - 128 : kCodeNone));
+        }
+        tmem_st16(tm.tm_k + 32 * j, wv);
+        tmem_st16(tm.tm_k + 32 * j + 16, cv);
     }
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     return base;
@@ -520,7 +543,9 @@ FCW_DI void tx_short_half(const KParams& P, const Team& tm, const SymDev& sy, co
         done += pair ? 2 * tm.nwarp : tm.nwarp;
         const bool act = i < gcount;
         if (!pair && !act) break;  // warp-uniform in the tail
-        const int m = act ? (P.grp_sub ? __ldg(&P.grp_sub[gstart + i]) : gstart + i) : gstart;
+        // (an idle half repeats the group's last subband: same TMEM row as its partner)
+        const int ic = min(i, gcount - 1);
+        const int m = P.grp_sub ? __ldg(&P.grp_sub[gstart + ic]) : gstart + ic;
         const SubDev sd = P.sub[m];
         const int2* ce = P.cls + sd.cls_off + t;
         float2 v[PPT];
@@ -604,6 +629,28 @@ FCW_DI void tx_short_half(const KParams& P, const Team& tm, const SymDev& sy, co
                 u, buf, stw, t, 0, tw16_of(P, stw), tm.tm_a);
             float2* spec = r ? spec1 : spec0;
             const float sgn = r ? sd.bp1 : 1.f;
+            if constexpr (tmem_tw_half<N, ZV>()) {
+                // weights and slot codes of this lane's bins from the class rows in TMEM: no table
+                // load and a short decode between the DFT and its stores
+                unsigned wv[16], cv[16];
+                const unsigned row = tm.tm_k + 32 * sd.row_tx;  // warp-uniform by plan construction
+                FCW_ASSERT(__shfl_sync(0xffffffffu, sd.row_tx, 0) == sd.row_tx);
+                tmem_ld16(row, wv);
+                tmem_ld16(row + 16, cv);
+                tmem_wait16(wv);
+                tmem_wait16(cv);
+                const int extm = ext0 - kCodeExt;
+                static_for<PPT>([&](auto kc) {
+                    constexpr int K = decltype(kc)::value;
+                    if constexpr (!((kZ6 >> K) & 1ull)) {
+                        const int code = (int)cv[K];
+                        const int dest = code >= kCodeExt ? extm + code : ((sd.c + code) & (N - 1));
+                        FCW_ASSERT(code >= kCodeNone || dest < P.spec_stride);
+                        if (act && code < kCodeNone) spec[dest] = cscale(u[K], __uint_as_float(wv[K]) * sgn);
+                    }
+                });
+                return;
+            }
             static_for<PPT>([&](auto kc) {
                 constexpr int K = decltype(kc)::value;
                 constexpr int KP = K ^ (PPT / 2);  // (t + 16K) ^ (L/2) == t + 16*KP
@@ -1158,7 +1205,9 @@ FCW_DI void rx_short_half(const KParams& P, const Team& tm, const SymDev& sy, co
         const int i = done + 2 * tm.warp + h;
         done += 2 * tm.nwarp;
         const bool act = i < gcount;
-        const int m = act ? (P.grp_sub ? __ldg(&P.grp_sub[gstart + i]) : gstart + i) : gstart;
+        // (an idle half repeats the group's last subband: same TMEM row as its partner)
+        const int ic = min(i, gcount - 1);
+        const int m = P.grp_sub ? __ldg(&P.grp_sub[gstart + ic]) : gstart + ic;
         const SubDev sd = P.sub[m];
         const int2* ce = P.cls + sd.cls_off + t;
         const int q0 = (sd.c - L / 2 + t) & (N - 1);
@@ -1166,13 +1215,21 @@ FCW_DI void rx_short_half(const KParams& P, const Team& tm, const SymDev& sy, co
         const float2* s1 = spec1 + q0;
         const float sig = sgn_t * sd.bp1;
         float2 f[PPT], gw[PPT];
+        unsigned wv[16];
+        if constexpr (tmem_tw_half<N, ZV>()) {
+            FCW_ASSERT(__shfl_sync(0xffffffffu, sd.row_rx, 0) == sd.row_rx);
+            tmem_ld16(tm.tm_k + 32 * sd.row_rx, wv);  // this lane's window weights (class row in TMEM)
+            tmem_wait16(wv);
+        }
         static_for<PPT>([&](auto kc) {
             constexpr int K = decltype(kc)::value;
             constexpr int KP = K ^ (PPT / 2);  // (t + 16K) ^ (L/2) == t + 16*KP
             if constexpr (ZV == 1 && ((kZ6 >> K) & 1ull)) {
                 gw[K] = zero2();  // outside every window: zero input, inactive output
             } else {
-                const float w = __int_as_float(__ldg(&ce[TW * K]).y);
+                float w;
+                if constexpr (tmem_tw_half<N, ZV>()) w = __uint_as_float(wv[K]);
+                else w = __int_as_float(__ldg(&ce[TW * K]).y);
                 const float2 a = s0[TW * KP], b = s1[TW * KP];
                 gw[K] = cscale(b, w);
                 f[K] = cscale(make_float2(fmaf(-sig, b.x, a.x), fmaf(-sig, b.y, a.y)), w);

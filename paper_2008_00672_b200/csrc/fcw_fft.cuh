@@ -300,7 +300,7 @@ FCW_DI void fft_reg(float2 (&x)[L]) {
 #define FCW_TMEM_TW 3
 #endif
 constexpr int kTwTmem = 99;      // TWL value: long-transform twiddles from TMEM
-constexpr int kTmemCols = 128;   // columns per CTA: sets A, B (32 each), C for warps 0-3 / 4-7 (32 each)
+constexpr int kTmemCols = 256;   // columns per CTA: sets A, B (32 each), C for warps 0-3 / 4-7 (32 each), 4 x 32 bin-class rows
 #define FCW_R16(a, o) a(o + 0), a(o + 1), a(o + 2), a(o + 3), a(o + 4), a(o + 5), a(o + 6), a(o + 7), a(o + 8), \
                       a(o + 9), a(o + 10), a(o + 11), a(o + 12), a(o + 13), a(o + 14), a(o + 15)
 FCW_DI void tmem_st16(unsigned taddr, const unsigned (&d)[16]) {

@@ -19,6 +19,7 @@ constexpr int kMaxN = 4096;       // long transform envelope (SMEM-resident bloc
 constexpr int kMaxL = 1024;       // short transform envelope (warp-resident)
 constexpr int kMaxGroups = 9;     // distinct L values: 4..1024
 constexpr int kMaxLevels = 8;     // contributor ranks per shared bin
+constexpr int kMaxTmemClasses = 4; // bin classes whose per-lane rows fit the TMEM columns of a zv kernel
 
 // Per-subband constants resident in HBM (read through L1).
 struct SubDev {
@@ -32,7 +33,10 @@ struct SubDev {
     float rx_s0;     // sqrt(I) (L/N) / sqrt(L)  (fc_sync.cpp:238-240)
     int cls_off;     // offset of this subband's bin-class row in the class table
     int ext_base;    // first extension slot of this subband's secondary bins
-    int pad_[3];
+    // zv kernels: the TMEM bin-class row pair this subband's warp reads in TX / RX (KParams::combo);
+    // both half-warps of a warp issue one tcgen05.ld, so the two subbands of a pair share the id
+    int row_tx, row_rx;
+    int pad_[1];
 };
 
 // Per-symbol geometry (all integer-exact on the host).
@@ -67,6 +71,10 @@ struct KParams {
     int accumulate;      // TX: add into the waveform instead of storing (FCW_TX_ACCUMULATE)
     int dbg_skip;        // dev-only timing knob (FCW_DEBUG_SKIP): 1 = short stage, 2 = long transform
     int n_ext, n_zero, n_lvl;
+    // zv kernels: TMEM bin-class rows.  Row j holds class combo[j][h] for the lanes of half-warp h
+    // (the pairs of classes that the fixed subband-to-warp schedule puts side by side in one warp)
+    int n_combo;
+    int combo[kMaxTmemClasses][2];
     int lvl_start[kMaxLevels + 1];
     int n_groups;
     int grp_L[kMaxGroups], grp_start[kMaxGroups], grp_count[kMaxGroups];
@@ -116,6 +124,7 @@ struct Plan {
     std::vector<float> h_win;
     std::vector<int> h_inv, h_dest, h_grp_sub, h_fix, h_zero;
     std::vector<int2> h_cls;
+    std::vector<int> h_combo;  // zv plans: flattened (class of half 0, class of half 1) per TMEM row
     std::vector<int> h_fix_slot;
     int n_ext = 0, n_lvl = 0;
     std::vector<int> lvl_start;

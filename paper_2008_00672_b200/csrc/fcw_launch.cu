@@ -304,6 +304,9 @@ void fill_common(const Plan& p, KParams& kp) {
     kp.n_zero = (p.zv || p.nb) ? p.n_zero_core : (int)p.h_zero.size();
     kp.nb_k0 = p.nb_k0;
     kp.n_lvl = p.n_lvl;
+    kp.n_combo = (int)p.h_combo.size() / 2;
+    for (int j = 0; j < kMaxTmemClasses; ++j)
+        for (int h = 0; h < 2; ++h) kp.combo[j][h] = j < kp.n_combo ? p.h_combo[2 * j + h] : 0;
     for (int i = 0; i <= kMaxLevels; ++i) kp.lvl_start[i] = i < (int)p.lvl_start.size() ? p.lvl_start[i] : p.n_ext;
     kp.n_groups = p.n_groups;
     for (int g = 0; g < kMaxGroups; ++g) {
