@@ -121,6 +121,17 @@ FCW_DI int theta_exp(int cmodN, int smodN) {
 
 FCW_DI float2 zero2() { return make_float2(0.f, 0.f); }
 
+// e^{+-2 pi i e / N} computed (sincospif of the exact fp32 argument 2 e / N, within an ulp of the
+// plan table's rounded double values) instead of a dependent load from the N-entry table: the
+// TX symbol rotator is needed once per subband-symbol at the head of its chain (TX 6.43 -> 6.34 ms;
+// at the tail of the RX chain the load is already hidden: RX 4.17 -> 4.20 ms, kept as a load).
+template <int N, int SIGN>
+FCW_DI float2 unit_phasor(int e) {
+    float sn, cs;
+    sincospif((float)e * (2.0f / (float)N), &sn, &cs);
+    return make_float2(cs, SIGN > 0 ? sn : -sn);
+}
+
 // *p += v as one fire-and-forget L2 reduction (red.global.add.v2.f32, sm_90+):
 // FCW_TX_ACCUMULATE adds each sample exactly once onto the stored waveform,
 // so the result equals the load-add-store it replaces, bit for bit.
@@ -566,7 +577,7 @@ FCW_DI void tx_short_half(const KParams& P, const Team& tm, const SymDev& sy, co
             }
         } else {
         {
-            const float2 ph = cscale(tw_conj(P.tw, theta_exp<N>(sd.cmodN, sy.smodN)), sd.tx_scale);
+            const float2 ph = cscale(unit_phasor<N, +1>(theta_exp<N>(sd.cmodN, sy.smodN)), sd.tx_scale);
             constexpr unsigned long long ZI = ZV == 1 ? kZ6 : 0ull;
             auto live = [&](int k) { return !((ZI >> k) & 1ull); };
             int inv[PPT];
