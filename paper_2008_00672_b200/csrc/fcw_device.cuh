@@ -121,6 +121,16 @@ FCW_DI int theta_exp(int cmodN, int smodN) {
 
 FCW_DI float2 zero2() { return make_float2(0.f, 0.f); }
 
+// spec[slot] = v under a predicate, as ONE predicated st.shared (no branch around the store and
+// the products that feed it); sbase = the spectrum's shared-space byte address.
+FCW_DI void sts_if(unsigned sbase, int slot, float2 v, bool pred) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t@p st.shared.v2.f32 [%0], {%1, %2};\n\t}" ::"r"(
+            sbase + 8u * (unsigned)slot),
+        "f"(v.x), "f"(v.y), "r"(0), "r"((int)pred)
+        : "memory");
+}
+
 // e^{+-2 pi i e / N} computed (sincospif of the exact fp32 argument 2 e / N, within an ulp of the
 // plan table's rounded double values) instead of a dependent load from the N-entry table: the
 // TX symbol rotator is needed once per subband-symbol at the head of its chain (TX 6.43 -> 6.34 ms;
@@ -651,13 +661,14 @@ FCW_DI void tx_short_half(const KParams& P, const Team& tm, const SymDev& sy, co
                 tmem_wait16(wv);
                 tmem_wait16(cv);
                 const int extm = ext0 - kCodeExt;
+                const unsigned sbase = (unsigned)__cvta_generic_to_shared(spec);
                 static_for<PPT>([&](auto kc) {
                     constexpr int K = decltype(kc)::value;
                     if constexpr (!((kZ6 >> K) & 1ull)) {
                         const int code = (int)cv[K];
                         const int dest = code >= kCodeExt ? extm + code : ((sd.c + code) & (N - 1));
                         FCW_ASSERT(code >= kCodeNone || dest < P.spec_stride);
-                        if (act && code < kCodeNone) spec[dest] = cscale(u[K], __uint_as_float(wv[K]) * sgn);
+                        sts_if(sbase, dest, cscale(u[K], __uint_as_float(wv[K]) * sgn), act && code < kCodeNone);
                     }
                 });
                 return;
