@@ -142,6 +142,24 @@ FCW_DI float2 unit_phasor(int e) {
     return make_float2(cs, SIGN > 0 ? sn : -sn);
 }
 
+// Predicated global stores as single instructions (no branch around the store and the
+// arithmetic that feeds it): streaming (.cs), plain, and the L2 reduction.
+FCW_DI void stcs_if(float2* p, float2 v, bool pred) {
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %3, 0;\n\t@p st.global.cs.v2.f32 [%0], {%1, %2};\n\t}" ::"l"(p),
+                 "f"(v.x), "f"(v.y), "r"((int)pred)
+                 : "memory");
+}
+FCW_DI void stg_if(float2* p, float2 v, bool pred) {
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %3, 0;\n\t@p st.global.v2.f32 [%0], {%1, %2};\n\t}" ::"l"(p),
+                 "f"(v.x), "f"(v.y), "r"((int)pred)
+                 : "memory");
+}
+FCW_DI void red_add2_if(float2* p, float2 v, bool pred) {
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %3, 0;\n\t@p red.global.add.v2.f32 [%0], {%1, %2};\n\t}" ::"l"(p),
+                 "f"(v.x), "f"(v.y), "r"((int)pred)
+                 : "memory");
+}
+
 // *p += v as one fire-and-forget L2 reduction (red.global.add.v2.f32, sm_90+):
 // FCW_TX_ACCUMULATE adds each sample exactly once onto the stored waveform,
 // so the result equals the load-add-store it replaces, bit for bit.
@@ -283,6 +301,7 @@ FCW_DI void tmem_release(unsigned base) {
 template <int N, int L, bool TDIO = true>  // TDIO: time-domain input compiled in (continuous FC)
 FCW_DI void tx_short_thread(const KParams& P, const Team& tm, const SymDev& sy, const float2* __restrict__ row,
                             float2* spec0, float2* spec1, int gstart, int gcount) {
+    const unsigned sb0 = (unsigned)__cvta_generic_to_shared(spec0), sb1 = (unsigned)__cvta_generic_to_shared(spec1);
     for (int i = tm.tid; i < gcount; i += tm.nthr) {
         const int m = P.grp_sub ? __ldg(&P.grp_sub[gstart + i]) : gstart + i;
         const SubDev sd = P.sub[m];
@@ -316,11 +335,9 @@ FCW_DI void tx_short_thread(const KParams& P, const Team& tm, const SymDev& sy, 
 #pragma unroll
         for (int b = 0; b < L; ++b) {
             const Bin e = bin_entry<N, L>(P, sd, b);
-            if (e.dest >= 0) {
-                FCW_ASSERT(e.dest < P.spec_stride);
-                spec0[e.dest] = cscale(u0[b], e.w);
-                spec1[e.dest] = cscale(u1[b], e.w * sd.bp1);
-            }
+            FCW_ASSERT(e.dest < P.spec_stride);
+            sts_if(sb0, max(e.dest, 0), cscale(u0[b], e.w), e.dest >= 0);  // predicated stores, no branch
+            sts_if(sb1, max(e.dest, 0), cscale(u1[b], e.w * sd.bp1), e.dest >= 0);
         }
     }
 }
@@ -331,6 +348,7 @@ FCW_DI void tx_short_thread(const KParams& P, const Team& tm, const SymDev& sy, 
 template <int N, int L>
 FCW_DI void tx_short_warp_lockstep(const KParams& P, const Team& tm, const SymDev& sy, const float2* __restrict__ row,
                           float2* spec0, float2* spec1, float2* scr, const float2* stw, int gstart, int gcount) {
+    const unsigned sb0 = (unsigned)__cvta_generic_to_shared(spec0), sb1 = (unsigned)__cvta_generic_to_shared(spec1);
     constexpr int PPT = L / 32;
     const int lane = threadIdx.x & 31;
     const int sts = P.stab_len / L;
@@ -404,11 +422,9 @@ FCW_DI void tx_short_warp_lockstep(const KParams& P, const Team& tm, const SymDe
         auto scatter = [&](auto kc) {
             constexpr int K = decltype(kc)::value;
             const BinW e = bin_warp<N, L, K>(ent[K], qbase, ext0);
-            if (e.dest >= 0) {
-                FCW_ASSERT(e.dest < P.spec_stride);
-                spec0[e.dest] = cscale(uu[0][K], e.w);
-                spec1[e.dest] = cscale(uu[1][K], e.w * bp1);
-            }
+            FCW_ASSERT(e.dest < P.spec_stride);
+            sts_if(sb0, max(e.dest, 0), cscale(uu[0][K], e.w), e.dest >= 0);  // predicated stores, no branch
+            sts_if(sb1, max(e.dest, 0), cscale(uu[1][K], e.w * bp1), e.dest >= 0);
         };
         static_for<PPT>(scatter);
     }
@@ -474,6 +490,7 @@ template <int N, int L, bool TDIO = true>  // TDIO: time-domain input compiled i
 FCW_DI void tx_short_warp(const KParams& P, const Team& tm, const SymDev& sy, const float2* __restrict__ row,
                           const float2* __restrict__ row_next, bool staged, float2* spec0, float2* spec1,
                           float2* scr, const float2* stw, int gstart, int gcount) {
+    const unsigned sb0 = (unsigned)__cvta_generic_to_shared(spec0), sb1 = (unsigned)__cvta_generic_to_shared(spec1);
     constexpr int PPT = L / 32;
     const int lane = threadIdx.x & 31;
     const int sts = P.stab_len / L;
@@ -529,7 +546,7 @@ FCW_DI void tx_short_warp(const KParams& P, const Team& tm, const SymDev& sy, co
                 constexpr int K = decltype(kc)::value;
                 const BinW e = bin_warp<N, L, K>(__ldg(&ce[32 * K]), qbase, ext0);
                 FCW_ASSERT(e.dest < P.spec_stride);
-                if (e.dest >= 0) spec[e.dest] = cscale(uu[r][K], e.w * sgn);
+                sts_if(r == 0 ? sb0 : sb1, max(e.dest, 0), cscale(uu[r][K], e.w * sgn), e.dest >= 0);
             });
         }
     }
@@ -761,6 +778,7 @@ FCW_DI void lane_fft16(float2 (&v)[NV], int b, const float2* __restrict__ tw) {
 template <int N>
 FCW_DI void tx_short_lanes16(const KParams& P, const Team& tm, const SymDev& sy, const float2* __restrict__ row,
                              float2* spec0, float2* spec1) {
+    const unsigned sb0 = (unsigned)__cvta_generic_to_shared(spec0), sb1 = (unsigned)__cvta_generic_to_shared(spec1);
     constexpr int L = 16;
     const int b = tm.tid & 15;
     for (int i0 = (tm.tid >> 5) * 2; i0 < P.M; i0 += tm.nthr / 16) {  // warp-uniform: two groups per warp
@@ -783,11 +801,9 @@ FCW_DI void tx_short_lanes16(const KParams& P, const Team& tm, const SymDev& sy,
         if (!((b >= L / 4 - lcp) && (b < 3 * L / 4))) u[0] = zero2();
         if (!((b >= L / 4) && (b < 3 * L / 4))) u[1] = zero2();
         lane_fft16<N, -1, 2>(u, b, P.tw);
-        if (act && e.dest >= 0) {
-            FCW_ASSERT(e.dest < P.spec_stride);
-            spec0[e.dest] = cscale(u[0], e.w);
-            spec1[e.dest] = cscale(u[1], e.w * sd.bp1);
-        }
+        FCW_ASSERT(e.dest < P.spec_stride);
+        sts_if(sb0, max(e.dest, 0), cscale(u[0], e.w), act && e.dest >= 0);  // predicated stores, no branch
+        sts_if(sb1, max(e.dest, 0), cscale(u[1], e.w * sd.bp1), act && e.dest >= 0);
     }
 }
 
@@ -1686,16 +1702,14 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU, ZV>()) tx_kernel(cons
                     if (mm < 16) val = v[0][mm];
                     if (mm >= 8) val = cadd(val, v[1][mm - 8]);
                     if (mm < 8) val = cadd(val, cr[mm]);
-                    if (u < sy.own_len) {
-                        if (emit) {
-                            FCW_ASSERT(sy.sigma + u < P.Q);
-                            if (P.accumulate) red_add2(&dst[u], val);  // L2-side add, no load latency
-                            else __stcs(&dst[u], val);  // streaming: the waveform is not re-read here (-1.4%)
-                        }
-                    } else {
-                        FCW_ASSERT(u - sy.own_len < N / 2);
-                        carry[u - sy.own_len] = val;
-                    }
+                    // predicated single-instruction stores: the owned span goes to the waveform
+                    // (streaming; an L2-side add under FCW_TX_ACCUMULATE), the rest to the carry
+                    const bool own = u < sy.own_len;
+                    FCW_ASSERT(!(own && emit) || sy.sigma + u < P.Q);
+                    FCW_ASSERT(own || u - sy.own_len < N / 2);
+                    if (P.accumulate) red_add2_if(&dst[u], val, own && emit);
+                    else stcs_if(&dst[u], val, own && emit);
+                    stg_if(&carry[own ? 0 : u - sy.own_len], val, !own);
                 }
             }
         }
