@@ -1704,12 +1704,13 @@ __global__ void __launch_bounds__(kThreads, min_blocks<LU, ZV>()) tx_kernel(cons
                     if (mm < 8) val = cadd(val, cr[mm]);
                     // predicated single-instruction stores: the owned span goes to the waveform
                     // (streaming; an L2-side add under FCW_TX_ACCUMULATE), the rest to the carry
-                    const bool own = u < sy.own_len;
+                    // (own_len = N + N_CP,n+1 >= N: the first 16 elements of a thread are always owned)
+                    const bool own = mm < 16 || u < sy.own_len;
                     FCW_ASSERT(!(own && emit) || sy.sigma + u < P.Q);
                     FCW_ASSERT(own || u - sy.own_len < N / 2);
                     if (P.accumulate) red_add2_if(&dst[u], val, own && emit);
                     else stcs_if(&dst[u], val, own && emit);
-                    stg_if(&carry[own ? 0 : u - sy.own_len], val, !own);
+                    if (mm >= 16) stg_if(&carry[own ? 0 : u - sy.own_len], val, !own);
                 }
             }
         }
