@@ -131,17 +131,6 @@ FCW_DI void sts_if(unsigned sbase, int slot, float2 v, bool pred) {
         : "memory");
 }
 
-// e^{+-2 pi i e / N} computed (sincospif of the exact fp32 argument 2 e / N, within an ulp of the
-// plan table's rounded double values) instead of a dependent load from the N-entry table: the
-// TX symbol rotator is needed once per subband-symbol at the head of its chain (TX 6.43 -> 6.34 ms;
-// at the tail of the RX chain the load is already hidden: RX 4.17 -> 4.20 ms, kept as a load).
-template <int N, int SIGN>
-FCW_DI float2 unit_phasor(int e) {
-    float sn, cs;
-    sincospif((float)e * (2.0f / (float)N), &sn, &cs);
-    return make_float2(cs, SIGN > 0 ? sn : -sn);
-}
-
 // Predicated global stores as single instructions (no branch around the store and the
 // arithmetic that feeds it): streaming (.cs), plain, and the L2 reduction.
 FCW_DI void stcs_if(float2* p, float2 v, bool pred) {
@@ -604,7 +593,12 @@ FCW_DI void tx_short_half(const KParams& P, const Team& tm, const SymDev& sy, co
             }
         } else {
         {
-            const float2 ph = cscale(unit_phasor<N, +1>(theta_exp<N>(sd.cmodN, sy.smodN)), sd.tx_scale);
+            // theta_n from the two-level SMEM table of the long transform (W^e = W^(64 h) W^l: two
+            // LDS and a product) instead of a dependent global table load at the head of the chain
+            // (TX 6.43 -> 6.34 ms; the RX chain reads it at its tail, where the load is hidden)
+            const int te = theta_exp<N>(sd.cmodN, sy.smodN);
+            const float2* ltw = stw + P.stab_len;
+            const float2 ph = cscale(cconj(cmul(ltw[64 + (te >> 6)], ltw[te & 63])), sd.tx_scale);
             constexpr unsigned long long ZI = ZV == 1 ? kZ6 : 0ull;
             auto live = [&](int k) { return !((ZI >> k) & 1ull); };
             int inv[PPT];
