@@ -446,6 +446,22 @@ int fcw_plan_create(fcw_plan** out, int N, double overlap, const int* cp_high, i
         p->h_fix.push_back(secondary[k].q);
         p->h_fix_slot.push_back(k);
     }
+    {
+        // grouped by the thread that loads the target bin in the long transform (q mod N/16):
+        // that thread adds its bins' secondary contributions, in rank order, right before it
+        // loads them (tx_kernel), so the fix-up needs no phase and no barrier of its own
+        const int T = std::max(1, N / 16);
+        std::vector<int> by_owner(order);
+        std::stable_sort(by_owner.begin(), by_owner.end(),
+                         [&](int a, int b) { return secondary[a].q % T < secondary[b].q % T; });
+        p->h_own_start.assign(T + 1, 0);
+        for (int k : by_owner) {
+            p->h_own_tgt.push_back(secondary[k].q);
+            p->h_own_slot.push_back(k);
+            ++p->h_own_start[secondary[k].q % T + 1];
+        }
+        for (int t = 0; t < T; ++t) p->h_own_start[t + 1] += p->h_own_start[t];
+    }
     p->lvl_start.assign(max_rank + 1, 0);
     for (int l = 0; l <= max_rank; ++l) {
         int k = 0;
@@ -617,6 +633,12 @@ int fcw_plan_create(fcw_plan** out, int N, double overlap, const int* cp_high, i
     off = align(off + sizeof(int) * std::max<size_t>(1, p->h_fix.size()));
     const size_t o_zero = off;
     off = align(off + sizeof(int) * std::max<size_t>(1, p->h_zero.size()));
+    const size_t o_ostart = off;
+    off = align(off + sizeof(int) * p->h_own_start.size());
+    const size_t o_otgt = off;
+    off = align(off + sizeof(int) * std::max<size_t>(1, p->h_own_tgt.size()));
+    const size_t o_oslot = off;
+    off = align(off + sizeof(int) * std::max<size_t>(1, p->h_own_slot.size()));
     const size_t o_tw = off;
     off = align(off + sizeof(float2) * N);
     std::vector<unsigned char> host(off, 0);
@@ -629,6 +651,11 @@ int fcw_plan_create(fcw_plan** out, int N, double overlap, const int* cp_high, i
     std::memcpy(&host[o_grp], p->h_grp_sub.data(), sizeof(int) * p->h_grp_sub.size());
     if (!p->h_fix.empty()) std::memcpy(&host[o_fix], p->h_fix.data(), sizeof(int) * p->h_fix.size());
     if (!p->h_zero.empty()) std::memcpy(&host[o_zero], p->h_zero.data(), sizeof(int) * p->h_zero.size());
+    std::memcpy(&host[o_ostart], p->h_own_start.data(), sizeof(int) * p->h_own_start.size());
+    if (!p->h_own_tgt.empty()) {
+        std::memcpy(&host[o_otgt], p->h_own_tgt.data(), sizeof(int) * p->h_own_tgt.size());
+        std::memcpy(&host[o_oslot], p->h_own_slot.data(), sizeof(int) * p->h_own_slot.size());
+    }
     std::memcpy(&host[o_tw], tw.data(), sizeof(float2) * N);
     cudaError_t e = cudaMalloc(&p->d_blob, off);
     if (e != cudaSuccess) {
@@ -650,6 +677,9 @@ int fcw_plan_create(fcw_plan** out, int N, double overlap, const int* cp_high, i
     p->d_grp_sub = reinterpret_cast<int*>(base + o_grp);
     p->d_fix = reinterpret_cast<int*>(base + o_fix);
     p->d_zero = reinterpret_cast<int*>(base + o_zero);
+    p->d_own_start = reinterpret_cast<int*>(base + o_ostart);
+    p->d_own_tgt = reinterpret_cast<int*>(base + o_otgt);
+    p->d_own_slot = reinterpret_cast<int*>(base + o_oslot);
     p->d_tw = reinterpret_cast<float2*>(base + o_tw);
     // SMEM envelope check (one CTA must fit)
     int dev_smem = 0;

@@ -89,6 +89,11 @@ struct KParams {
     const int* grp_sub;  // subband ids grouped by L
     const int* fix_tgt;  // [n_ext] target bin of each secondary contribution, rank-ordered
     const int* fix_slot; // [n_ext] its extension slot
+    // the same contributions grouped by the long-transform thread that loads the target bin
+    // (q mod N/16), rank order kept inside a group: entries [own_start[t], own_start[t + 1])
+    const int* own_start;
+    const int* own_tgt;
+    const int* own_slot;
     const int* zero_list;  // [n_zero] bins no subband touches
     const float2* tw;    // [N] exp(-2 pi i k / N)
     // time-domain I/O of the continuous FC (fcw_cont.cu, cp = 0 plans; null =
@@ -126,6 +131,7 @@ struct Plan {
     std::vector<int2> h_cls;
     std::vector<int> h_combo;  // zv plans: flattened (class of half 0, class of half 1) per TMEM row
     std::vector<int> h_fix_slot;
+    std::vector<int> h_own_start, h_own_tgt, h_own_slot;  // fix-up list grouped by owner thread
     int n_ext = 0, n_lvl = 0;
     std::vector<int> lvl_start;
     int n_groups = 0;
@@ -144,6 +150,7 @@ struct Plan {
     int *d_inv = nullptr, *d_grp_sub = nullptr, *d_fix = nullptr, *d_zero = nullptr;
     int2* d_cls = nullptr;
     int* d_fix_slot = nullptr;
+    int *d_own_start = nullptr, *d_own_tgt = nullptr, *d_own_slot = nullptr;
     float2* d_tw = nullptr;
     // host-buffer pipeline state
     std::mutex host_mu;

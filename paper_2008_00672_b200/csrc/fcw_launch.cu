@@ -323,6 +323,9 @@ void fill_common(const Plan& p, KParams& kp) {
     // uniform-L plans iterate subbands directly (identity group order)
     kp.grp_sub = uniform_L(p) ? nullptr : p.d_grp_sub;
     kp.fix_tgt = p.d_fix;
+    kp.own_start = p.d_own_start;
+    kp.own_tgt = p.d_own_tgt;
+    kp.own_slot = p.d_own_slot;
     kp.zero_list = p.d_zero;
     kp.tw = p.d_tw;
     kp.stab_len = stab_len(p);
