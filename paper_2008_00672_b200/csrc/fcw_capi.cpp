@@ -95,7 +95,7 @@ void pick_schedule(const fcw::Plan& p, int S, bool tx, fcw::KParams& kp) {
     const bool force_static = sched && std::strcmp(sched, "static") == 0;
     if (!kp.dynamic && per_team >= 200 && !force_static) {
         kp.dynamic = 1;
-        kp.chunk = std::min(p.B, tx ? 140 : 16);  // measured (tools/tools_sched.sh): TX 28 -> 140 is -1%
+        kp.chunk = std::min(p.B, tx ? 140 : 28);  // measured (tools/ab.sh): TX 28 -> 140 is -1%; RX 16 -> 28 is -0.8%
     }
     kp.nchunks = (p.B + kp.chunk - 1) / kp.chunk;
 }
