@@ -80,6 +80,8 @@ typedef struct fcw_plan_info {
     int row_full;          /* full grid row length: sum_m L_m */
     int N_L, N_T;
     int chunk;             /* symbols per CTA (launch geometry, informational) */
+    int kernel_variant;    /* informational: 0 general, 1 zero-bin L = 256 / N = 4096 (TMEM tables), 2 narrowband, 3 team-only */
+    int tmem_rows;         /* zero-bin variant: bin-class row pairs parked in tensor memory (<= 4) */
 } fcw_plan_info;
 
 /* ----------------------------------------------------------------- plan */

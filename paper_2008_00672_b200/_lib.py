@@ -58,7 +58,8 @@ class SubbandC(C.Structure):
 class PlanInfoC(C.Structure):
     _fields_ = [("N", C.c_int), ("B", C.c_int), ("M", C.c_int), ("overlap", C.c_double), ("Q", C.c_int64),
                 ("useful0", C.c_int64), ("frame_samples", C.c_int64), ("row_active", C.c_int),
-                ("row_full", C.c_int), ("N_L", C.c_int), ("N_T", C.c_int), ("chunk", C.c_int)]
+                ("row_full", C.c_int), ("N_L", C.c_int), ("N_T", C.c_int), ("chunk", C.c_int),
+                ("kernel_variant", C.c_int), ("tmem_rows", C.c_int)]
 
 
 _lib = None

@@ -248,6 +248,8 @@ class Plan:
         self.row_full = int(info.row_full)
         self.N_L, self.N_T = int(info.N_L), int(info.N_T)
         self.chunk = int(info.chunk)
+        # informational: 0 general, 1 zero-bin (TMEM tables), 2 narrowband, 3 team-only kernels
+        self.kernel_variant, self.tmem_rows = int(info.kernel_variant), int(info.tmem_rows)
 
     def close(self) -> None:
         if getattr(self, "_h", None):

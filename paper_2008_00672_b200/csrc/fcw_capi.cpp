@@ -724,6 +724,8 @@ int fcw_plan_get_info(const fcw_plan* p, fcw_plan_info* info) {
     info->N_L = p->pN.N_L;
     info->N_T = p->pN.N_T;
     info->chunk = p->chunk;
+    info->kernel_variant = p->zv ? 1 : (p->nb ? 2 : (fcw::plan_team_only(*p) ? 3 : 0));
+    info->tmem_rows = p->zv ? (int)p->h_combo.size() / 2 : 0;
     return FCW_OK;
 }
 

@@ -195,6 +195,7 @@ cudaError_t launch_tx(const Plan& plan, KParams& kp, int S, cudaStream_t st);
 cudaError_t launch_rx(const Plan& plan, KParams& kp, int S, cudaStream_t st);
 cudaError_t launch_gen_qam(const Plan& plan, uint64_t seed, long long unit0, int S, int bits,
                            float2* out, cudaStream_t st);
+bool plan_team_only(const Plan& plan);  // the plan runs the team-only kernels (fcw_launch.cu)
 size_t tx_smem_bytes(const Plan& plan);
 // fcw_link.cu (link step around the path; blocking where results go to the host)
 cudaError_t link_stats(const Plan& p, const float2* grid, long long stride, int S, uint64_t seed, long long unit0,

@@ -339,6 +339,8 @@ void fill_common(const Plan& p, KParams& kp) {
 #endif
 }
 
+// 0 general, 2 narrowband, 1 zero-bin, 3 team-only: the kernel family `pick` selects (informational)
+bool plan_team_only(const Plan& p) { return team_only(p); }
 size_t tx_smem_bytes(const Plan& p) { return smem_bytes(p, true, false); }
 size_t rx_smem_bytes(const Plan& p) { return smem_bytes(p, false, true); }
 

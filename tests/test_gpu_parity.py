@@ -218,6 +218,52 @@ def test_random_geometries(N, Ls, cps):
             assert rel_rms(out[u], want_p) <= TOL, (u, fused)
 
 
+def _zv_case(n_acts, cs, n_tb=4):
+    """Uniform L = 256 at N = 4096 with centred active maps and design_window windows: the
+    structure the zero-bin (zv) kernels accept."""
+    subs, maps = [], []
+    for n_act, c in zip(n_acts, cs):
+        subs.append(api.SubbandConfig(L=256, c=c, window=api.design_window(256, n_act, n_tb)))
+        maps.append(api.centered_active_map(256, n_act, skip_dc=False))
+    return subs, maps
+
+
+@pytest.mark.parametrize("n_acts,cs,variant", [
+    # three classes whose pairs differ between TX (one subband per warp) and RX (pairs (0,1), (2,-))
+    ([144, 108, 144], [600, 1500, 3200], 1),
+    # adjacent subbands sharing transition bins, a narrower one in the middle: mixed class pairs
+    ([144, 144, 120, 144, 144], [400, 552, 700, 848, 1000], None),
+    # ten subbands of six widths: more class pairs than TMEM rows -> the plan falls back to the general kernels
+    ([144, 132, 120, 108, 96, 84, 144, 132, 120, 108], [300 + 160 * i for i in range(10)], 0),
+])
+def test_zero_bin_plans_with_mixed_classes(n_acts, cs, variant):
+    """zv plans keep per-lane (weight, slot code) rows of their bin classes in TMEM, one row per
+    PAIR of classes that the schedule puts in one warp (fcw_capi.cpp); plans needing more than
+    four rows must fall back.  Either way the results match the oracle."""
+    N, cps = 4096, [352, 288, 288, 288, 288]
+    subs, maps = _zv_case(n_acts, cs)
+    rng = np.random.default_rng(sum(n_acts))
+    B = len(cps)
+    plan = api.Plan(N, cps, subs, maps)
+    if variant is not None:
+        assert plan.kernel_variant == variant, (plan.kernel_variant, plan.tmem_rows)
+    assert plan.tmem_rows <= 4
+    S = 2
+    grid = (rng.standard_normal((S, B, plan.row_active)) + 1j * rng.standard_normal((S, B, plan.row_active)))
+    grid = grid.astype(np.complex64)
+    wave = plan.tx_host(grid, S)
+    w = type("W", (), {})()
+    w.subbands, w.active_maps, w.B, w.N, w.cp = subs, maps, B, N, cps
+    for u in range(S):
+        want, u0 = oracle_tx(w, grid[u].astype(np.complex128))
+        assert rel_rms(wave[u], want) <= TOL, u
+    for fused in (False, True):
+        out = plan.rx_host(wave, plan.Q, plan.useful0, S, fused=fused)
+        for u in range(S):
+            want_p, _ = oracle_rx(w, wave[u].astype(np.complex128), plan.useful0, fused)
+            assert rel_rms(out[u], want_p) <= TOL, (u, fused)
+
+
 def test_kernel_smem_attribute_across_plans():
     """One generic kernel, plans with more / less / more dynamic SMEM: the
     kernel's SMEM attribute must never be lowered under a larger plan (it was
