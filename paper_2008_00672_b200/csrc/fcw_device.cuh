@@ -606,8 +606,10 @@ FCW_DI void tx_short_half(const KParams& P, const Team& tm, const SymDev& sy, co
             for (int k = 0; k < PPT; ++k) {
                 if constexpr (ZV == 1) {
                     // zv plans have centred active maps: no table load ahead of the gather
+                    // (no `act` here: an idle half repeats the group's last subband in full, so its
+                    // scatter stores the same values as the half that owns that subband)
                     const int a = (t + TW * k + (sd.n_act >> 1)) & (L - 1);
-                    inv[k] = (act && live(k) && a < sd.n_act) ? a : -1;
+                    inv[k] = (live(k) && a < sd.n_act) ? a : -1;
                 } else {
                     inv[k] = (act && live(k)) ? (int)(short)(__ldg(&ce[TW * k]).x & 0xffff) : -1;
                 }
@@ -679,7 +681,7 @@ FCW_DI void tx_short_half(const KParams& P, const Team& tm, const SymDev& sy, co
                         const int code = (int)cv[K];
                         const int dest = code >= kCodeExt ? extm + code : ((sd.c + code) & (N - 1));
                         FCW_ASSERT(code >= kCodeNone || dest < P.spec_stride);
-                        sts_if(sbase, dest, cscale(u[K], __uint_as_float(wv[K]) * sgn), act && code < kCodeNone);
+                        sts_if(sbase, dest, cscale(u[K], __uint_as_float(wv[K]) * sgn), code < kCodeNone);  // (idle halves repeat the last subband)
                     }
                 });
                 return;
@@ -1279,7 +1281,8 @@ FCW_DI void rx_short_half(const KParams& P, const Team& tm, const SymDev& sy, co
             return make_float2(fmaf(f[k].x, P1.x, fmaf(-f[k].y, P1.y, fmaf(gw[k].x, P2.x, -gw[k].y * P2.y))),
                                fmaf(f[k].x, P1.y, fmaf(f[k].y, P1.x, fmaf(gw[k].x, P2.y, gw[k].y * P2.x))));
         };
-        if (act) {
+        // (an idle half repeats its partner's subband: it stores the same values to the same places)
+        {
             if (P.grid_full) {
                 float2* o = orow + sd.full_off + t;
 #pragma unroll

@@ -233,6 +233,8 @@ def _zv_case(n_acts, cs, n_tb=4):
     ([144, 108, 144], [600, 1500, 3200], 1),
     # adjacent subbands sharing transition bins, a narrower one in the middle: mixed class pairs
     ([144, 144, 120, 144, 144], [400, 552, 700, 848, 1000], None),
+    # ten adjacent equal subbands: a TX pair round with idle half-warps (slots 10..15 repeat the last subband)
+    ([144] * 10, [200 + 144 * i for i in range(10)], 1),
     # ten subbands of six widths: more class pairs than TMEM rows -> the plan falls back to the general kernels
     ([144, 132, 120, 108, 96, 84, 144, 132, 120, 108], [300 + 160 * i for i in range(10)], 0),
 ])
